@@ -1,0 +1,156 @@
+/*
+ * hgr_cuda.h -- C ABI of the B200-native hierarchical refactoring library
+ * (libhgr_b200.so, sources in paper_2007_04457_b200/csrc/).
+ *
+ * Drop-in boundary for the reference's hot path. The reference (`hgr`,
+ * header-only C++20, /root/reference/proj/include/hgr) has no FFI of its own;
+ * its public entry points are C++ templates. Each function below states the
+ * reference interface it replaces (file:line, relative to proj/include/hgr/).
+ * The C++ template drop-in that re-declares the reference API on top of this
+ * ABI is include/hgr_b200/hgr.hpp; the Python mirror is
+ * paper_2007_04457_b200/__init__.py.
+ *
+ * Conventions
+ *  - Arrays are row-major, last dimension contiguous (ndarray.hpp:15-57), rank 1..3.
+ *  - "d_" pointers are device pointers (cudaMalloc'd or torch tensors) on the
+ *    current CUDA device; "h_" pointers are host pointers.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device-pointer calls are stream-ordered and asynchronous unless noted.
+ *  - Every call returns an hgr_status; on failure hgr_cuda_last_error() (thread
+ *    local) holds a message whose substrings match the reference's hgr::error
+ *    texts ("2^k+1", "non-finite", "zero at coarse", "level out of range",
+ *    "class index out of range", "shape").
+ */
+#ifndef HGR_CUDA_H
+#define HGR_CUDA_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGR_CUDA_ABI_VERSION 1
+
+typedef enum hgr_status {
+  HGR_OK = 0,
+  HGR_ERR_INVALID = 1,   /* argument/shape/level validation (reference: detail::require) */
+  HGR_ERR_CUDA = 2,      /* CUDA runtime failure */
+  HGR_ERR_NONFINITE = 3, /* decompose input held NaN/Inf (refactor.hpp:36-38) */
+  HGR_ERR_NOMEM = 4
+} hgr_status;
+
+typedef enum hgr_dtype { HGR_F32 = 0, HGR_F64 = 1 } hgr_dtype;
+
+/* Grid description = the arguments of GridHierarchy(coords_per_dim)
+ * (grid_hierarchy.hpp:51-70) / GridHierarchy::uniform (:73-80).
+ * coords[d] may be NULL for uniform integer coordinates 0..n-1. */
+typedef struct hgr_grid_desc {
+  int rank;
+  size_t extents[3];
+  const double* coords[3];
+} hgr_grid_desc;
+
+typedef struct hgr_plan_s* hgr_plan;
+
+const char* hgr_cuda_last_error(void);
+int hgr_cuda_abi_version(void);
+
+/* ---- plans: GridHierarchy + device tables + workspace ---------------------
+ * Replaces GridHierarchy construction (grid_hierarchy.hpp:51-70, build_caches
+ * :163-188) and the per-call workspace of correction_level (correction.hpp:301).
+ * A plan is immutable after creation and may be shared by host threads that
+ * use distinct streams only if they do not run concurrently on it (the
+ * workspace is per plan); create one plan per stream for concurrency. */
+int hgr_cuda_plan_create(const hgr_grid_desc* grid, int dtype, hgr_plan* out);
+void hgr_cuda_plan_destroy(hgr_plan plan);
+/* GridHierarchy::levels() (grid_hierarchy.hpp:85) */
+int hgr_cuda_plan_levels(hgr_plan plan);
+/* bytes of device workspace held by the plan */
+size_t hgr_cuda_plan_workspace_bytes(hgr_plan plan);
+/* number of kernel launches one decompose/recompose enqueues */
+int hgr_cuda_plan_launches(hgr_plan plan, int direction /*0 dec, 1 rec*/, int upto_class);
+
+/* decompose (refactor.hpp:32-57): in place on the finest-shape device array.
+ * Non-finite inputs are detected inside the first kernel; the outcome is
+ * reported by hgr_cuda_plan_sync_status (d_data is then unspecified, the
+ * reference's by-value input is preserved by the host/C++ layers). */
+int hgr_cuda_plan_decompose(hgr_plan plan, void* d_data, void* stream);
+/* recompose (refactor.hpp:63-90): classes 0..upto_class; d_out may equal d_in. */
+int hgr_cuda_plan_recompose(hgr_plan plan, const void* d_in, void* d_out, int upto_class,
+                            void* stream);
+/* synchronizes `stream`; returns HGR_ERR_NONFINITE if the last decompose saw NaN/Inf */
+int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream);
+
+/* ---- one-shot entry points (plan cached by grid + dtype) --------------------
+ * C-ABI twins of hgr::decompose<T> / hgr::recompose<T> (refactor.hpp:32-33, :63-64). */
+int hgr_cuda_decompose_f64(const hgr_grid_desc* grid, double* d_data, void* stream);
+int hgr_cuda_decompose_f32(const hgr_grid_desc* grid, float* d_data, void* stream);
+int hgr_cuda_recompose_f64(const hgr_grid_desc* grid, const double* d_in, double* d_out,
+                           int upto_class, void* stream);
+int hgr_cuda_recompose_f32(const hgr_grid_desc* grid, const float* d_in, float* d_out,
+                           int upto_class, void* stream);
+
+/* Host-pointer convenience (synchronous: H2D, run, D2H). This is what the
+ * C++ template drop-in (include/hgr_b200/hgr.hpp) calls. decompose checks
+ * finiteness before touching h_data (refactor.hpp:36-38). */
+int hgr_decompose_host_f64(const hgr_grid_desc* grid, double* h_data);
+int hgr_decompose_host_f32(const hgr_grid_desc* grid, float* h_data);
+int hgr_recompose_host_f64(const hgr_grid_desc* grid, const double* h_in, double* h_out,
+                           int upto_class);
+int hgr_recompose_host_f32(const hgr_grid_desc* grid, const float* h_in, float* h_out,
+                           int upto_class);
+
+/* ---- single-level entry points (known-answer-test surface) -----------------
+ * Compact level arrays (extents of level `level` / `level-1`), device pointers,
+ * synchronous. */
+/* interpolate_to_fine (transforms.hpp:76-92) */
+int hgr_cuda_interpolate_to_fine_f64(const hgr_grid_desc* g, int level, const double* d_coarse,
+                                     double* d_fine, void* stream);
+int hgr_cuda_interpolate_to_fine_f32(const hgr_grid_desc* g, int level, const float* d_coarse,
+                                     float* d_fine, void* stream);
+/* compute_coefficients (transforms.hpp:96-111) */
+int hgr_cuda_compute_coefficients_f64(const hgr_grid_desc* g, int level, const double* d_fine,
+                                      double* d_coeffs, void* stream);
+int hgr_cuda_compute_coefficients_f32(const hgr_grid_desc* g, int level, const float* d_fine,
+                                      float* d_coeffs, void* stream);
+/* compute_correction (correction.hpp:348-365); rejects nonzero coarse entries */
+int hgr_cuda_compute_correction_f64(const hgr_grid_desc* g, int level, const double* d_coeffs,
+                                    double* d_z, void* stream);
+int hgr_cuda_compute_correction_f32(const hgr_grid_desc* g, int level, const float* d_coeffs,
+                                    float* d_z, void* stream);
+
+/* ---- class packing (refactor.hpp:134-170) ----------------------------------
+ * extract_class / scatter_class on the finest-shape pyramid, device pointers.
+ * d_values holds class_node_count(cls) values in the reference's row-major order. */
+int hgr_cuda_extract_class_f64(const hgr_grid_desc* g, const double* d_data, int cls,
+                               double* d_values, void* stream);
+int hgr_cuda_extract_class_f32(const hgr_grid_desc* g, const float* d_data, int cls,
+                               float* d_values, void* stream);
+int hgr_cuda_scatter_class_f64(const hgr_grid_desc* g, double* d_data, int cls,
+                               const double* d_values, void* stream);
+int hgr_cuda_scatter_class_f32(const hgr_grid_desc* g, float* d_data, int cls,
+                               const float* d_values, void* stream);
+/* GridHierarchy::class_node_count (grid_hierarchy.hpp:146-150); 0 on error */
+size_t hgr_class_node_count(const hgr_grid_desc* g, int cls);
+/* GridHierarchy levels (grid_hierarchy.hpp:51-70); -1 on error */
+int hgr_levels(const hgr_grid_desc* g);
+
+/* ---- fiber operators (correction.hpp:58-223), batched over `count` fibers --
+ * d_v: count fibers of length n (contiguous, fiber-major); d_h: n-1 spacings
+ * shared by all fibers. Outputs: mass n, transfer/masstrans (n-1)/2+1, thomas n. */
+int hgr_cuda_mass_apply_f64(size_t n, size_t count, const double* d_v, const double* h_h,
+                            double* d_out, void* stream);
+int hgr_cuda_masstrans_apply_f64(size_t n, size_t count, const double* d_v, const double* h_h,
+                                 double* d_out, void* stream);
+int hgr_cuda_thomas_solve_f64(size_t n, size_t count, const double* d_rhs, const double* h_h,
+                              double* d_out, void* stream);
+int hgr_cuda_masstrans_apply_f32(size_t n, size_t count, const float* d_v, const float* h_h,
+                                 float* d_out, void* stream);
+int hgr_cuda_thomas_solve_f32(size_t n, size_t count, const float* d_rhs, const float* h_h,
+                              float* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGR_CUDA_H */

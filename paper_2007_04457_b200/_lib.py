@@ -1,0 +1,79 @@
+"""ctypes binding of the C ABI in include/hgr_cuda.h (libhgr_b200.so).
+
+There is deliberately no fallback: if the CUDA library is missing the import
+fails loudly. Build it with ``__graft_entry__.build()`` or
+``make -C paper_2007_04457_b200/csrc``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhgr_b200.so"
+
+HGR_OK, HGR_ERR_INVALID, HGR_ERR_CUDA, HGR_ERR_NONFINITE, HGR_ERR_NOMEM = 0, 1, 2, 3, 4
+HGR_F32, HGR_F64 = 0, 1
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("rank", C.c_int), ("extents", C.c_size_t * 3), ("coords", C.c_void_p * 3)]
+
+
+_vp, _sz, _int = C.c_void_p, C.c_size_t, C.c_int
+_G = C.POINTER(GridDesc)
+
+_SIGS = {
+    "hgr_cuda_last_error": (C.c_char_p, []),
+    "hgr_cuda_abi_version": (_int, []),
+    "hgr_cuda_plan_create": (_int, [_G, _int, C.POINTER(_vp)]),
+    "hgr_cuda_plan_destroy": (None, [_vp]),
+    "hgr_cuda_plan_levels": (_int, [_vp]),
+    "hgr_cuda_plan_workspace_bytes": (_sz, [_vp]),
+    "hgr_cuda_plan_launches": (_int, [_vp, _int, _int]),
+    "hgr_cuda_plan_decompose": (_int, [_vp, _vp, _vp]),
+    "hgr_cuda_plan_recompose": (_int, [_vp, _vp, _vp, _int, _vp]),
+    "hgr_cuda_plan_sync_status": (_int, [_vp, _vp]),
+    "hgr_class_node_count": (_sz, [_G, _int]),
+    "hgr_levels": (_int, [_G]),
+}
+for _t in ("f64", "f32"):
+    _SIGS.update({
+        f"hgr_cuda_decompose_{_t}": (_int, [_G, _vp, _vp]),
+        f"hgr_cuda_recompose_{_t}": (_int, [_G, _vp, _vp, _int, _vp]),
+        f"hgr_decompose_host_{_t}": (_int, [_G, _vp]),
+        f"hgr_recompose_host_{_t}": (_int, [_G, _vp, _vp, _int]),
+        f"hgr_cuda_interpolate_to_fine_{_t}": (_int, [_G, _int, _vp, _vp, _vp]),
+        f"hgr_cuda_compute_coefficients_{_t}": (_int, [_G, _int, _vp, _vp, _vp]),
+        f"hgr_cuda_compute_correction_{_t}": (_int, [_G, _int, _vp, _vp, _vp]),
+        f"hgr_cuda_extract_class_{_t}": (_int, [_G, _vp, _int, _vp, _vp]),
+        f"hgr_cuda_scatter_class_{_t}": (_int, [_G, _vp, _int, _vp, _vp]),
+        f"hgr_cuda_masstrans_apply_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
+        f"hgr_cuda_thomas_solve_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
+    })
+_SIGS["hgr_cuda_mass_apply_f64"] = (_int, [_sz, _sz, _vp, _vp, _vp, _vp])
+
+EXPORTED_SYMBOLS = tuple(sorted(_SIGS))
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libhgr_b200.so (raises if it was not built -- no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"hgr CUDA library not found at {LIB_PATH}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().hgr_cuda_last_error().decode()

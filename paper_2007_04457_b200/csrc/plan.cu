@@ -1,0 +1,446 @@
+// plan.cu -- host orchestration: hierarchy, device tables, workspace, and the
+// per-level launch schedule of decompose / recompose.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+
+namespace hgrb {
+
+// ---- Hierarchy (grid_hierarchy.hpp:51-188) ------------------------------------
+
+Hierarchy Hierarchy::from_desc(const hgr_grid_desc* g) {
+  require(g != nullptr, "grid descriptor is null");
+  require(g->rank >= 1 && g->rank <= 3, "grid must have 1 to 3 dimensions");
+  Hierarchy h;
+  h.rank = g->rank;
+  h.coords.resize(std::size_t(g->rank));
+  int min_depth = -1;
+  for (int d = 0; d < g->rank; ++d) {
+    const std::size_t n = g->extents[d];
+    require(n >= 2 && ((n - 1) & (n - 2)) == 0,
+            "dimension size must be 2^k+1 (dimension " + std::to_string(d) + " has " +
+                std::to_string(n) + " nodes)");
+    auto& c = h.coords[std::size_t(d)];
+    c.resize(n);
+    for (std::size_t i = 0; i < n; ++i) c[i] = g->coords[d] ? g->coords[d][i] : double(i);
+    for (std::size_t i = 0; i + 1 < n; ++i)
+      require(c[i] < c[i + 1],
+              "coordinates must be strictly increasing (dimension " + std::to_string(d) + ")");
+    int depth = 0;
+    for (std::size_t v = n - 1; !(v & 1); v >>= 1) ++depth;
+    if (min_depth < 0 || depth < min_depth) min_depth = depth;
+  }
+  h.L = min_depth;
+  return h;
+}
+
+std::size_t Hierarchy::node_count(int l) const {
+  std::size_t n = 1;
+  for (int d = 0; d < rank; ++d) n *= extent(l, d);
+  return n;
+}
+
+std::size_t Hierarchy::class_node_count(int cls) const {
+  require(cls >= 0 && cls <= L, "level out of range");
+  return cls == 0 ? node_count(0) : node_count(cls) - node_count(cls - 1);
+}
+
+std::vector<double> Hierarchy::spacings(int l, int d) const {
+  const std::size_t s = stride(l);
+  const auto& c = coords[std::size_t(d)];
+  std::vector<double> h((c.size() - 1) / s);
+  for (std::size_t i = 0; i < h.size(); ++i) h[i] = c[(i + 1) * s] - c[i * s];
+  return h;
+}
+
+void Hierarchy::canon_extents(int l, int64_t e[3]) const {
+  e[0] = e[1] = e[2] = 1;
+  for (int d = 0; d < rank; ++d) e[d + 3 - rank] = int64_t(extent(l, d));
+}
+
+int Plan::sync_status(cudaStream_t s) {
+  HGR_CUDA_CHECK(cudaMemcpyAsync(h_flag_, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HGR_CUDA_CHECK(cudaStreamSynchronize(s));
+  return *h_flag_ ? HGR_ERR_NONFINITE : HGR_OK;
+}
+
+// ---- precision-specific plan ----------------------------------------------------
+
+namespace {
+
+// MassTransOperator<T> taps (correction.hpp:96-133), computed in T exactly as
+// the reference does (spacings cast to T, refined_node_weights in T).
+template <class T>
+std::vector<T> masstrans_taps(const std::vector<T>& h) {
+  const std::size_t nf = h.size() + 1, nc = (nf - 1) / 2 + 1;
+  auto main_ = [&](std::size_t i) {
+    const T left = i > 0 ? h[i - 1] : T(0);
+    const T right = i + 1 < nf ? h[i] : T(0);
+    return T(2) * (left + right);
+  };
+  auto mass_entry = [&](std::size_t t, std::size_t j) -> T {
+    if (j == t) return main_(t);
+    if (j + 1 == t) return h[t - 1];
+    if (j == t + 1) return h[t];
+    return T(0);
+  };
+  std::vector<T> taps(nc * 5, T(0));
+  for (std::size_t i = 0; i < nc; ++i) {
+    std::size_t rj[3];
+    T rw[3];
+    std::size_t rn = 0;
+    if (i > 0) {
+      const T span = h[2 * i - 2] + h[2 * i - 1];
+      rj[rn] = 2 * i - 1;
+      rw[rn++] = h[2 * i - 2] / span;  // to_right
+    }
+    rj[rn] = 2 * i;
+    rw[rn++] = T(1);
+    if (i + 1 < nc) {
+      const T span = h[2 * i] + h[2 * i + 1];
+      rj[rn] = 2 * i + 1;
+      rw[rn++] = h[2 * i + 1] / span;  // to_left
+    }
+    for (std::size_t k = 0; k < 5; ++k) {
+      const long j = long(2 * i) - 2 + long(k);
+      if (j < 0 || j >= long(nf)) continue;
+      T sum = T(0);
+      for (std::size_t r = 0; r < rn; ++r) sum += rw[r] * mass_entry(rj[r], std::size_t(j));
+      taps[i * 5 + k] = sum;
+    }
+  }
+  return taps;
+}
+
+// ThomasSolver<T> factors (correction.hpp:188-198)
+template <class T>
+void thomas_factors(const std::vector<T>& h, std::vector<T>& mult, std::vector<T>& pivot,
+                    std::vector<T>& upper, std::vector<T>& rpiv) {
+  const std::size_t n = h.size() + 1;
+  auto main_ = [&](std::size_t i) {
+    const T left = i > 0 ? h[i - 1] : T(0);
+    const T right = i + 1 < n ? h[i] : T(0);
+    return T(2) * (left + right);
+  };
+  pivot.assign(n, T(0));
+  mult.assign(n > 1 ? n - 1 : 1, T(0));
+  upper.assign(n > 1 ? n - 1 : 1, T(0));
+  rpiv.assign(n, T(0));
+  for (std::size_t i = 0; i < n; ++i) pivot[i] = main_(i);
+  for (std::size_t i = 0; i + 1 < n; ++i) upper[i] = h[i];
+  for (std::size_t i = 1; i < n; ++i) {
+    mult[i - 1] = h[i - 1] / pivot[i - 1];
+    pivot[i] = main_(i) - mult[i - 1] * upper[i - 1];
+  }
+  for (std::size_t i = 0; i < n; ++i) rpiv[i] = T(1) / pivot[i];
+}
+
+template <class T>
+class PlanT final : public Plan {
+ public:
+  explicit PlanT(const Hierarchy& hier);
+  ~PlanT() override;
+
+  void decompose(void* d_data, cudaStream_t s) override;
+  void recompose(const void* d_in, void* d_out, int upto, cudaStream_t s) override;
+  int launches(int direction, int upto) override;
+  std::size_t workspace_bytes() const override { return ws_bytes_; }
+  void interpolate_to_fine(int level, const void* coarse, void* fine, cudaStream_t s) override;
+  void compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) override;
+  void compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) override;
+  void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) override;
+
+ private:
+  void correction(int l, const T* in, T* z, T* apply, int sign, cudaStream_t s);
+  bool fused_ok(int l) const;
+  int L() const { return h.L; }
+
+  std::vector<LevelArgs<T>> args_;     // index l = 1..L (0 unused)
+  std::vector<std::array<int64_t, 3>> ext_;  // canonical extents per level 0..L
+  std::vector<T*> C_;                  // compact level arrays 0..L-1
+  std::vector<T*> Z_;                  // corrections 1..L
+  T* stage_[2] = {nullptr, nullptr};
+  char* tables_ = nullptr;
+  char* ws_ = nullptr;
+  std::size_t ws_bytes_ = 0;
+  int launch_count_ = 0;
+};
+
+template <class T>
+PlanT<T>::PlanT(const Hierarchy& hier) {
+  h = hier;
+  dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
+  HGR_CUDA_CHECK(cudaGetDevice(&device));
+  const int rank = h.rank, Lv = h.L;
+  ext_.resize(std::size_t(Lv) + 1);
+  for (int l = 0; l <= Lv; ++l) h.canon_extents(l, ext_[std::size_t(l)].data());
+
+  // -- host tables, packed into one device allocation
+  std::vector<char> blob;
+  auto push = [&](const std::vector<T>& v) {
+    std::size_t off = (blob.size() + 255) & ~std::size_t(255);
+    blob.resize(off + v.size() * sizeof(T));
+    std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  };
+  struct Off {
+    std::size_t wl, wr, taps, mult, pivot, upper, rpiv;
+  };
+  std::vector<std::array<Off, 3>> offs(std::size_t(Lv) + 1);
+  for (int l = 1; l <= Lv; ++l) {
+    for (int d = 0; d < rank; ++d) {
+      const int k = d + 3 - rank;
+      Off o{};
+      const auto hf = h.spacings(l, d);
+      std::vector<T> wl(hf.size() / 2), wr(hf.size() / 2);
+      for (std::size_t q = 0; q < hf.size() / 2; ++q) {
+        const double span = hf[2 * q] + hf[2 * q + 1];
+        wl[q] = T(hf[2 * q + 1] / span);
+        wr[q] = T(hf[2 * q] / span);
+      }
+      o.wl = push(wl);
+      o.wr = push(wr);
+      std::vector<T> hT(hf.begin(), hf.end());
+      o.taps = push(masstrans_taps<T>(hT));
+      const auto hc = h.spacings(l - 1, d);
+      std::vector<T> hcT(hc.begin(), hc.end()), mult, pivot, upper, rpiv;
+      thomas_factors<T>(hcT, mult, pivot, upper, rpiv);
+      o.mult = push(mult);
+      o.pivot = push(pivot);
+      o.upper = push(upper);
+      o.rpiv = push(rpiv);
+      offs[std::size_t(l)][std::size_t(k)] = o;
+    }
+  }
+  if (!blob.empty()) {
+    HGR_CUDA_CHECK(cudaMalloc(&tables_, blob.size()));
+    HGR_CUDA_CHECK(cudaMemcpy(tables_, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+  }
+  args_.resize(std::size_t(Lv) + 1);
+  for (int l = 1; l <= Lv; ++l) {
+    LevelArgs<T>& a = args_[std::size_t(l)];
+    std::memset(&a, 0, sizeof a);
+    for (int k = 0; k < 3; ++k) {
+      a.e[k] = ext_[std::size_t(l)][std::size_t(k)];
+      a.c[k] = ext_[std::size_t(l) - 1][std::size_t(k)];
+      if (k < 3 - rank) continue;
+      const Off& o = offs[std::size_t(l)][std::size_t(k)];
+      auto P = [&](std::size_t off) { return reinterpret_cast<const T*>(tables_ + off); };
+      a.wl[k] = P(o.wl);
+      a.wr[k] = P(o.wr);
+      a.taps[k] = P(o.taps);
+      a.mult[k] = P(o.mult);
+      a.pivot[k] = P(o.pivot);
+      a.upper[k] = P(o.upper);
+      a.rpiv[k] = P(o.rpiv);
+    }
+  }
+
+  // -- workspace: compact level arrays C_0..C_{L-1}, corrections Z_1..Z_L, LPK stages
+  auto nelem = [&](int l) {
+    const auto& e = ext_[std::size_t(l)];
+    return std::size_t(e[0] * e[1] * e[2]);
+  };
+  std::size_t stage_n[2] = {0, 0};
+  for (int l = 1; l <= Lv; ++l) {
+    std::array<int64_t, 3> e = ext_[std::size_t(l)];
+    int pass = 0;
+    for (int k = 3 - rank; k < 2; ++k, ++pass) {  // all but the last pass write a stage
+      e[std::size_t(k)] = ext_[std::size_t(l) - 1][std::size_t(k)];
+      stage_n[pass & 1] = std::max(stage_n[pass & 1], std::size_t(e[0] * e[1] * e[2]));
+    }
+  }
+  std::vector<std::size_t> off_c(static_cast<std::size_t>(Lv)),
+      off_z(static_cast<std::size_t>(Lv) + 1);
+  std::size_t total = 0;
+  const std::size_t esz = sizeof(T);
+  for (int l = 0; l < Lv; ++l) {
+    off_c[std::size_t(l)] = total;
+    total += (nelem(l) * esz + 255) & ~std::size_t(255);
+  }
+  for (int l = 1; l <= Lv; ++l) {
+    off_z[std::size_t(l)] = total;
+    total += (nelem(l - 1) * esz + 255) & ~std::size_t(255);
+  }
+  const std::size_t off_s0 = total;
+  total += (stage_n[0] * esz + 255) & ~std::size_t(255);
+  const std::size_t off_s1 = total;
+  total += (stage_n[1] * esz + 255) & ~std::size_t(255);
+  ws_bytes_ = total;
+  if (total) HGR_CUDA_CHECK(cudaMalloc(&ws_, total));
+  C_.resize(std::size_t(Lv));
+  Z_.assign(std::size_t(Lv) + 1, nullptr);
+  for (int l = 0; l < Lv; ++l) C_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_c[std::size_t(l)]);
+  for (int l = 1; l <= Lv; ++l) Z_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_z[std::size_t(l)]);
+  stage_[0] = reinterpret_cast<T*>(ws_ + off_s0);
+  stage_[1] = reinterpret_cast<T*>(ws_ + off_s1);
+  HGR_CUDA_CHECK(cudaMalloc(&d_flag_, sizeof(int)));
+  HGR_CUDA_CHECK(cudaMemset(d_flag_, 0, sizeof(int)));
+  HGR_CUDA_CHECK(cudaMallocHost(&h_flag_, sizeof(int)));
+}
+
+template <class T>
+PlanT<T>::~PlanT() {
+  cudaFree(tables_);
+  cudaFree(ws_);
+  cudaFree(d_flag_);
+  cudaFreeHost(h_flag_);
+}
+
+// correction_level (correction.hpp:295-340): LPK passes over the real dims in
+// ascending order (mask on the first), then Thomas passes in ascending order;
+// the last Thomas pass optionally applies apply += sign*z instead of storing z.
+template <class T>
+void PlanT<T>::correction(int l, const T* in, T* z, T* apply, int sign, cudaStream_t s) {
+  const LevelArgs<T>& a = args_[std::size_t(l)];
+  const int rank = h.rank;
+  int64_t e[3] = {a.e[0], a.e[1], a.e[2]};
+  const T* cur = in;
+  int pass = 0;
+  for (int k = 3 - rank; k < 3; ++k, ++pass) {
+    T* dst = (k == 2) ? z : stage_[pass & 1];
+    launch_lpk<T>(cur, e, dst, k, a.c[k], a.taps[k], pass == 0, s);
+    ++launch_count_;
+    e[k] = a.c[k];
+    cur = dst;
+  }
+  for (int k = 3 - rank; k < 3; ++k) {
+    const bool last = k == 2;
+    launch_thomas<T>(z, e, k, a.mult[k], a.rpiv[k], a.upper[k], last ? apply : nullptr, sign, s);
+    ++launch_count_;
+  }
+}
+
+template <class T>
+bool PlanT<T>::fused_ok(int) const {
+  return false;
+}
+
+// decompose (refactor.hpp:32-57) on the compact-level schedule:
+//   levels L..1: GPK (coefficients in place + gather of the coarse nodes into
+//   C_{l-1}), correction of the coefficients, C_{l-1} += z (fused into the last
+//   Thomas pass); then the pyramid is assembled by writing each C_{l-1} back to
+//   the even positions of level l.
+template <class T>
+void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
+  T* data = static_cast<T*>(d_data);
+  launch_count_ = 0;
+  HGR_CUDA_CHECK(cudaMemsetAsync(d_flag_, 0, sizeof(int), s));
+  const int Lv = L();
+  if (Lv == 0) {
+    check_finite<T>(data, h.node_count(0), d_flag_, s);
+    ++launch_count_;
+    return;
+  }
+  auto level_ptr = [&](int l) { return l == Lv ? data : C_[std::size_t(l)]; };
+  for (int l = Lv; l >= 1; --l) {
+    launch_gpk_dec<T>(level_ptr(l), C_[std::size_t(l) - 1], args_[std::size_t(l)], d_flag_,
+                      l == Lv, s);
+    ++launch_count_;
+    correction(l, level_ptr(l), Z_[std::size_t(l)], C_[std::size_t(l) - 1], +1, s);
+  }
+  for (int l = 1; l <= Lv; ++l) {
+    launch_scatter_even<T>(C_[std::size_t(l) - 1], level_ptr(l), args_[std::size_t(l)], s);
+    ++launch_count_;
+  }
+}
+
+// recompose (refactor.hpp:63-90): corrections are computed top-down while the
+// coarse nodes are gathered into compact level arrays, then levels 1..L apply
+// coarse -= z and the interpolation (refined nodes = coef + interp).
+template <class T>
+void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
+  const T* in = static_cast<const T*>(d_in);
+  T* out = static_cast<T*>(d_out);
+  launch_count_ = 0;
+  const int Lv = L();
+  require(m >= 0 && m <= Lv, "recompose: class index out of range");
+  if (Lv == 0) {
+    if (out != in)
+      HGR_CUDA_CHECK(cudaMemcpyAsync(out, in, h.node_count(0) * sizeof(T),
+                                     cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  const auto& fe = ext_[std::size_t(Lv)];
+  if (m < Lv) {
+    launch_gather<T>(in, fe.data(), int64_t(1) << (Lv - m), C_[std::size_t(m)],
+                     ext_[std::size_t(m)].data(), s);
+    ++launch_count_;
+  }
+  for (int l = m; l >= 1; --l) {
+    const T* src = l == Lv ? in : C_[std::size_t(l)];
+    correction(l, src, Z_[std::size_t(l)], nullptr, 0, s);
+    launch_gather<T>(src, ext_[std::size_t(l)].data(), 2, C_[std::size_t(l) - 1],
+                     ext_[std::size_t(l) - 1].data(), s);
+    ++launch_count_;
+  }
+  for (int l = 1; l <= Lv; ++l) {
+    const bool with = l <= m;
+    const T* coef = l == Lv ? in : C_[std::size_t(l)];
+    T* dst = l == Lv ? out : C_[std::size_t(l)];
+    launch_gpk_rec<T>(coef, dst, C_[std::size_t(l) - 1], with ? Z_[std::size_t(l)] : nullptr,
+                      args_[std::size_t(l)], with, s);
+    ++launch_count_;
+  }
+}
+
+template <class T>
+int PlanT<T>::launches(int direction, int upto) {
+  // dry count: mirrors the schedule above
+  const int Lv = L(), rank = h.rank;
+  if (direction == 0) return Lv == 0 ? 1 : Lv * (1 + 2 * rank) + Lv;
+  if (Lv == 0) return 0;
+  return (upto < Lv ? 1 : 0) + upto * (2 * rank + 1) + Lv;
+}
+
+template <class T>
+void PlanT<T>::interpolate_to_fine(int level, const void* coarse, void* fine, cudaStream_t s) {
+  require(level >= 1 && level <= L(), "level out of range");
+  launch_interpolate<T>(static_cast<const T*>(coarse), static_cast<T*>(fine),
+                        args_[std::size_t(level)], s);
+}
+
+template <class T>
+void PlanT<T>::compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) {
+  require(level >= 1 && level <= L(), "level out of range");
+  launch_coefficients<T>(static_cast<const T*>(fine), static_cast<T*>(coeffs),
+                         args_[std::size_t(level)], s);
+}
+
+template <class T>
+void PlanT<T>::compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) {
+  require(level >= 1 && level <= L(), "level out of range");
+  HGR_CUDA_CHECK(cudaMemsetAsync(d_flag_, 0, sizeof(int), s));
+  launch_check_coarse_zero<T>(static_cast<const T*>(coeffs), args_[std::size_t(level)], d_flag_,
+                              s);
+  HGR_CUDA_CHECK(cudaMemcpyAsync(h_flag_, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HGR_CUDA_CHECK(cudaStreamSynchronize(s));
+  require(*h_flag_ == 0,
+          "compute_correction: coefficients must be zero at coarse-grid positions");
+  correction(level, static_cast<const T*>(coeffs), static_cast<T*>(z), nullptr, 0, s);
+}
+
+template <class T>
+void PlanT<T>::class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) {
+  require(cls >= 0 && cls <= L(), "level out of range");
+  launch_class_copy<T>(static_cast<T*>(data), ext_[std::size_t(L())].data(),
+                       int64_t(1) << (L() - cls), ext_[std::size_t(cls)].data(), cls == 0,
+                       static_cast<T*>(values), extract, s);
+}
+
+}  // namespace
+
+std::unique_ptr<Plan> make_plan(const hgr_grid_desc* g, int dtype) {
+  Hierarchy h = Hierarchy::from_desc(g);
+  if (dtype == HGR_F64) return std::make_unique<PlanT<double>>(h);
+  require(dtype == HGR_F32, "dtype must be HGR_F32 or HGR_F64");
+  return std::make_unique<PlanT<float>>(h);
+}
+
+}  // namespace hgrb

@@ -1,0 +1,79 @@
+// plan.hpp -- host-side orchestration (C++): grid hierarchy, per-level device
+// tables, device workspace and the per-level launch schedule.
+//
+// Mirrors the reference's host structures:
+//   Hierarchy            <- GridHierarchy (grid_hierarchy.hpp:47-194)
+//   PlanT<T>::decompose  <- hgr::decompose (refactor.hpp:32-57)
+//   PlanT<T>::recompose  <- hgr::recompose (refactor.hpp:63-90)
+//   PlanT<T>::correction <- detail::correction_level (correction.hpp:295-340)
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hgr_cuda.h"
+#include "common.cuh"
+
+namespace hgrb {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+inline void require(bool ok, const std::string& what, int code = HGR_ERR_INVALID) {
+  if (!ok) throw Error(code, what);
+}
+
+// GridHierarchy (grid_hierarchy.hpp:47-194) in reference dimension order.
+struct Hierarchy {
+  int rank = 0;
+  int L = 0;
+  std::vector<std::vector<double>> coords;
+
+  static Hierarchy from_desc(const hgr_grid_desc* g);
+  std::size_t stride(int l) const { return std::size_t{1} << unsigned(L - l); }
+  std::size_t extent(int l, int d) const { return (coords[d].size() - 1) / stride(l) + 1; }
+  std::size_t node_count(int l) const;
+  std::size_t class_node_count(int cls) const;
+  // spacings (grid_hierarchy.hpp:163-177)
+  std::vector<double> spacings(int l, int d) const;
+  // canonical (left-padded) extents of level l
+  void canon_extents(int l, int64_t e[3]) const;
+};
+
+// Kernel launch accounting (for bench's gpu_launches and the plan API).
+struct LaunchCounter {
+  int count = 0;
+};
+
+class Plan {
+ public:
+  virtual ~Plan() = default;
+  Hierarchy h;
+  int dtype = HGR_F64;
+  int device = 0;
+  virtual void decompose(void* d_data, cudaStream_t s) = 0;
+  virtual void recompose(const void* d_in, void* d_out, int upto, cudaStream_t s) = 0;
+  virtual int launches(int direction, int upto) = 0;
+  virtual std::size_t workspace_bytes() const = 0;
+  int sync_status(cudaStream_t s);
+
+  // single-level / packing entry points (compact level arrays)
+  virtual void interpolate_to_fine(int level, const void* coarse, void* fine, cudaStream_t s) = 0;
+  virtual void compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) = 0;
+  virtual void compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) = 0;
+  virtual void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) = 0;
+
+ protected:
+  int* d_flag_ = nullptr;   // non-finite flag set by the level-L decompose kernel
+  int* h_flag_ = nullptr;   // pinned mirror
+};
+
+std::unique_ptr<Plan> make_plan(const hgr_grid_desc* g, int dtype);
+
+}  // namespace hgrb
