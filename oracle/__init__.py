@@ -69,11 +69,11 @@ class Oracle:
             self.pfx = "hgrref_"
         else:
             raise ValueError(kind)
-        self.lib[self.pfx + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.pfx + "last_error").restype = C.c_char_p
 
     # -- plumbing ---------------------------------------------------------------
     def _fn(self, name):
-        return self.lib[self.pfx + name]
+        return getattr(self.lib, self.pfx + name)
 
     def _check(self, rc):
         if rc != 0:
