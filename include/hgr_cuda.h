@@ -76,6 +76,9 @@ int hgr_cuda_plan_launches(hgr_plan plan, int direction /*0 dec, 1 rec*/, int up
  * reported by hgr_cuda_plan_sync_status (d_data is then unspecified, the
  * reference's by-value input is preserved by the host/C++ layers). */
 int hgr_cuda_plan_decompose(hgr_plan plan, void* d_data, void* stream);
+/* decompose out of place: d_in is left untouched (the reference's by-value
+ * `decompose(ndarray<T> data, ...)`, refactor.hpp:32-33); fastest path. */
+int hgr_cuda_plan_decompose_to(hgr_plan plan, const void* d_in, void* d_out, void* stream);
 /* recompose (refactor.hpp:63-90): classes 0..upto_class; d_out may equal d_in. */
 int hgr_cuda_plan_recompose(hgr_plan plan, const void* d_in, void* d_out, int upto_class,
                             void* stream);
@@ -86,6 +89,10 @@ int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream);
  * C-ABI twins of hgr::decompose<T> / hgr::recompose<T> (refactor.hpp:32-33, :63-64). */
 int hgr_cuda_decompose_f64(const hgr_grid_desc* grid, double* d_data, void* stream);
 int hgr_cuda_decompose_f32(const hgr_grid_desc* grid, float* d_data, void* stream);
+int hgr_cuda_decompose_to_f64(const hgr_grid_desc* grid, const double* d_in, double* d_out,
+                              void* stream);
+int hgr_cuda_decompose_to_f32(const hgr_grid_desc* grid, const float* d_in, float* d_out,
+                              void* stream);
 int hgr_cuda_recompose_f64(const hgr_grid_desc* grid, const double* d_in, double* d_out,
                            int upto_class, void* stream);
 int hgr_cuda_recompose_f32(const hgr_grid_desc* grid, const float* d_in, float* d_out,

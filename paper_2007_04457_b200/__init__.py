@@ -223,6 +223,11 @@ class Plan:
         _check(_lib.load().hgr_cuda_plan_decompose(self._h, _ptr(data),
                                                    stream if stream is not None else _stream_of(data)))
 
+    def decompose_into(self, src, out, stream: Optional[int] = None) -> None:
+        """Out-of-place, stream-ordered decompose (src untouched; no sync)."""
+        _check(_lib.load().hgr_cuda_plan_decompose_to(self._h, _ptr(src), _ptr(out),
+                                                      stream if stream is not None else _stream_of(src)))
+
     def recompose_into(self, src, out, upto_class: int, stream: Optional[int] = None) -> None:
         _check(_lib.load().hgr_cuda_plan_recompose(self._h, _ptr(src), _ptr(out), int(upto_class),
                                                    stream if stream is not None else _stream_of(src)))
@@ -242,8 +247,10 @@ def decompose(data, g: GridHierarchy) -> RefactoredArray:
     t = _dtype_tag(data)
     lib = _lib.load()
     if _is_torch(data):
-        out = data.detach().clone().contiguous()
-        _check(getattr(lib, f"hgr_cuda_decompose_{t}")(C.byref(g.desc), _ptr(out), _stream_of(out)))
+        src = data.detach().contiguous()
+        out = src.new_empty(src.shape)
+        _check(getattr(lib, f"hgr_cuda_decompose_to_{t}")(C.byref(g.desc), _ptr(src), _ptr(out),
+                                                           _stream_of(src)))
     else:
         out = np.array(data, copy=True, order="C")
         _check(getattr(lib, f"hgr_decompose_host_{t}")(C.byref(g.desc), _ptr(out)))

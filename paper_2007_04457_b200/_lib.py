@@ -31,6 +31,7 @@ _SIGS = {
     "hgr_cuda_plan_workspace_bytes": (_sz, [_vp]),
     "hgr_cuda_plan_launches": (_int, [_vp, _int, _int]),
     "hgr_cuda_plan_decompose": (_int, [_vp, _vp, _vp]),
+    "hgr_cuda_plan_decompose_to": (_int, [_vp, _vp, _vp, _vp]),
     "hgr_cuda_plan_recompose": (_int, [_vp, _vp, _vp, _int, _vp]),
     "hgr_cuda_plan_sync_status": (_int, [_vp, _vp]),
     "hgr_class_node_count": (_sz, [_G, _int]),
@@ -39,6 +40,7 @@ _SIGS = {
 for _t in ("f64", "f32"):
     _SIGS.update({
         f"hgr_cuda_decompose_{_t}": (_int, [_G, _vp, _vp]),
+        f"hgr_cuda_decompose_to_{_t}": (_int, [_G, _vp, _vp, _vp]),
         f"hgr_cuda_recompose_{_t}": (_int, [_G, _vp, _vp, _int, _vp]),
         f"hgr_decompose_host_{_t}": (_int, [_G, _vp]),
         f"hgr_recompose_host_{_t}": (_int, [_G, _vp, _vp, _int]),

@@ -98,6 +98,16 @@ int decompose_dev(const hgr_grid_desc* g, T* d, void* stream) {
 }
 
 template <class T>
+int decompose_to_dev(const hgr_grid_desc* g, const T* in, T* out, void* stream) {
+  return guarded([&] {
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    p->decompose_to(in, out, as_stream(stream));
+    int st = p->sync_status(as_stream(stream));
+    if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
+  });
+}
+
+template <class T>
 int recompose_dev(const hgr_grid_desc* g, const T* in, T* out, int m, void* stream) {
   return guarded([&] {
     auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
@@ -117,14 +127,14 @@ int decompose_host(const hgr_grid_desc* g, T* h) {
   return guarded([&] {
     auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
     const std::size_t n = finest_count(*p);
-    DevBuf<T> d(n);
+    DevBuf<T> d(n), o(n);
     cudaStream_t s = nullptr;
     HGR_CUDA_CHECK(cudaMemcpy(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice));
-    // finiteness is validated before anything is modified (refactor.hpp:36-38)
-    p->decompose(d.p, s);
+    // finiteness is validated before h is modified (refactor.hpp:36-38)
+    p->decompose_to(d.p, o.p, s);
     int st = p->sync_status(s);
     if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
-    HGR_CUDA_CHECK(cudaMemcpy(h, d.p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    HGR_CUDA_CHECK(cudaMemcpy(h, o.p, n * sizeof(T), cudaMemcpyDeviceToHost));
   });
 }
 
@@ -292,6 +302,13 @@ int hgr_cuda_plan_decompose(hgr_plan plan, void* d_data, void* stream) {
   });
 }
 
+int hgr_cuda_plan_decompose_to(hgr_plan plan, const void* d_in, void* d_out, void* stream) {
+  return guarded([&] {
+    hgrb::require(plan != nullptr, "plan is null");
+    plan->plan->decompose_to(d_in, d_out, as_stream(stream));
+  });
+}
+
 int hgr_cuda_plan_recompose(hgr_plan plan, const void* d_in, void* d_out, int upto_class,
                             void* stream) {
   return guarded([&] {
@@ -312,6 +329,12 @@ int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream) {
 
 int hgr_cuda_decompose_f64(const hgr_grid_desc* g, double* d, void* s) { return decompose_dev(g, d, s); }
 int hgr_cuda_decompose_f32(const hgr_grid_desc* g, float* d, void* s) { return decompose_dev(g, d, s); }
+int hgr_cuda_decompose_to_f64(const hgr_grid_desc* g, const double* i, double* o, void* s) {
+  return decompose_to_dev(g, i, o, s);
+}
+int hgr_cuda_decompose_to_f32(const hgr_grid_desc* g, const float* i, float* o, void* s) {
+  return decompose_to_dev(g, i, o, s);
+}
 int hgr_cuda_recompose_f64(const hgr_grid_desc* g, const double* i, double* o, int m, void* s) {
   return recompose_dev(g, i, o, m, s);
 }

@@ -20,6 +20,9 @@ namespace hgrb {
 //  taps   : mass-trans stencil K = R*M, 5 per coarse row (correction.hpp:96-133), in T
 //  mult/pivot/upper/rpiv : Thomas factors of the level-(l-1) mass matrix
 //           (correction.hpp:188-198), in T; rpiv = 1/pivot
+//  h      : level-l spacings in T (spacings_as<T>, correction.hpp:227-231), e_d-1
+//  trl/trr: transfer weights in T (correction.hpp:67-88): weight of fine node
+//           2q-1 (trl) / 2q+1 (trr) into coarse node q, 0 at the ends; c_d entries
 template <class T>
 struct LevelArgs {
   int64_t e[3];  // level-l (fine) extents
@@ -27,6 +30,9 @@ struct LevelArgs {
   const T* wl[3];
   const T* wr[3];
   const T* taps[3];
+  const T* h[3];
+  const T* trl[3];
+  const T* trr[3];
   const T* mult[3];
   const T* pivot[3];
   const T* upper[3];

@@ -1,0 +1,41 @@
+// kernels_fused.cuh -- launchers of the bandwidth-optimised sm_100a kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace hgrb {
+
+// Batched Thomas solve of the level-(l-1) mass matrix along `dim` (IPK,
+// correction.hpp:202-208 / :262-278), out-of-place allowed (in may equal out).
+// Lines are split into chunks held in registers; the chunks are stitched with
+// an exact affine carry scan (the forward/backward recurrences are first-order
+// affine), then each chunk re-runs the reference recurrence from its true
+// carry. Returns false if the line length exceeds the register tiling (the
+// caller then uses the one-thread-per-line kernel).
+template <class T>
+bool launch_thomas_fast(const T* in, T* out, const int64_t ext[3], int dim, const T* mult,
+                        const T* rpiv, const T* upper, cudaStream_t s);
+
+enum FusedMode : int {
+  kFusedDecompose = 0,  // coefficients -> coef_out, K*U -> zload
+  kFusedLoadOnly = 1,   // K*U -> zload only
+  kFusedRecompose = 2   // K*(U masked at coarse nodes) -> zload, coarse nodes -> gather
+};
+
+// Fused level kernel (GPK + LPK on all dimensions): marches along dim 0 over
+// (dim1, dim2) tiles of the level-l array U; fine planes arrive in shared
+// memory through cp.async.bulk (TMA bulk-copy engine) into an mbarrier ring.
+// Returns false if the level is not supported (caller falls back).
+// flag (decompose mode, may be null): set to 1 if any input value is NaN/Inf.
+template <class T>
+bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
+                        int mode, int* flag, cudaStream_t s);
+
+// Recompose interpolation (GPK^-1, refactor.hpp:77-87): coarse = C - Z (Z may be
+// null), out[coarse] = coarse, out[refined] = (with ? coef : 0) + interp(coarse).
+// 3D tiles with the coarse block staged in shared memory. in-place safe.
+template <class T>
+bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
+                       bool with_coeffs, cudaStream_t s);
+
+}  // namespace hgrb

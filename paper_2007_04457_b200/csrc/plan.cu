@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "kernels_fused.cuh"
 #include "plan.hpp"
 
 namespace hgrb {
@@ -156,20 +157,26 @@ class PlanT final : public Plan {
   void compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) override;
   void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) override;
 
+  void decompose_to(const void* d_in, void* d_out, cudaStream_t s) override;
+
  private:
   void correction(int l, const T* in, T* z, T* apply, int sign, cudaStream_t s);
-  bool fused_ok(int l) const;
+  void thomas_all(int l, T* z, T* last_out, cudaStream_t s);
+  void decompose_level(int l, const T* src, T* coef_dst, bool in_place, cudaStream_t s);
+  bool big(int l) const { return h.node_count(l) >= (std::size_t(1) << 15); }
   int L() const { return h.L; }
 
   std::vector<LevelArgs<T>> args_;     // index l = 1..L (0 unused)
   std::vector<std::array<int64_t, 3>> ext_;  // canonical extents per level 0..L
   std::vector<T*> C_;                  // compact level arrays 0..L-1
+  std::vector<T*> D_;                  // compact coefficient arrays 1..L-1 (decompose)
   std::vector<T*> Z_;                  // corrections 1..L
   T* stage_[2] = {nullptr, nullptr};
   char* tables_ = nullptr;
   char* ws_ = nullptr;
   std::size_t ws_bytes_ = 0;
   int launch_count_ = 0;
+  int last_launches_[2] = {0, 0};
 };
 
 template <class T>
@@ -190,7 +197,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
     return off;
   };
   struct Off {
-    std::size_t wl, wr, taps, mult, pivot, upper, rpiv;
+    std::size_t wl, wr, taps, mult, pivot, upper, rpiv, h, trl, trr;
   };
   std::vector<std::array<Off, 3>> offs(std::size_t(Lv) + 1);
   for (int l = 1; l <= Lv; ++l) {
@@ -208,6 +215,18 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
       o.wr = push(wr);
       std::vector<T> hT(hf.begin(), hf.end());
       o.taps = push(masstrans_taps<T>(hT));
+      o.h = push(hT);
+      {
+        // transfer weights in T (refined_node_weights<T>, correction.hpp:76-84)
+        const std::size_t nc = hT.size() / 2 + 1;
+        std::vector<T> trl(nc, T(0)), trr(nc, T(0));
+        for (std::size_t q = 0; q < nc; ++q) {
+          if (q > 0) trl[q] = hT[2 * q - 2] / (hT[2 * q - 2] + hT[2 * q - 1]);
+          if (q + 1 < nc) trr[q] = hT[2 * q + 1] / (hT[2 * q] + hT[2 * q + 1]);
+        }
+        o.trl = push(trl);
+        o.trr = push(trr);
+      }
       const auto hc = h.spacings(l - 1, d);
       std::vector<T> hcT(hc.begin(), hc.end()), mult, pivot, upper, rpiv;
       thomas_factors<T>(hcT, mult, pivot, upper, rpiv);
@@ -239,6 +258,9 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
       a.pivot[k] = P(o.pivot);
       a.upper[k] = P(o.upper);
       a.rpiv[k] = P(o.rpiv);
+      a.h[k] = P(o.h);
+      a.trl[k] = P(o.trl);
+      a.trr[k] = P(o.trr);
     }
   }
 
@@ -249,6 +271,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   };
   std::size_t stage_n[2] = {0, 0};
   for (int l = 1; l <= Lv; ++l) {
+    if (big(l)) continue;  // fused levels need no LPK stage buffers
     std::array<int64_t, 3> e = ext_[std::size_t(l)];
     int pass = 0;
     for (int k = 3 - rank; k < 2; ++k, ++pass) {  // all but the last pass write a stage
@@ -257,12 +280,17 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
     }
   }
   std::vector<std::size_t> off_c(static_cast<std::size_t>(Lv)),
-      off_z(static_cast<std::size_t>(Lv) + 1);
+      off_z(static_cast<std::size_t>(Lv) + 1), off_d(static_cast<std::size_t>(Lv) + 1);
   std::size_t total = 0;
   const std::size_t esz = sizeof(T);
+  // +256 B slack per buffer: bulk copies of the last row may round up to 16 B
   for (int l = 0; l < Lv; ++l) {
     off_c[std::size_t(l)] = total;
-    total += (nelem(l) * esz + 255) & ~std::size_t(255);
+    total += (nelem(l) * esz + 511) & ~std::size_t(255);
+  }
+  for (int l = 1; l < Lv; ++l) {
+    off_d[std::size_t(l)] = total;
+    total += (nelem(l) * esz + 511) & ~std::size_t(255);
   }
   for (int l = 1; l <= Lv; ++l) {
     off_z[std::size_t(l)] = total;
@@ -277,6 +305,8 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   C_.resize(std::size_t(Lv));
   Z_.assign(std::size_t(Lv) + 1, nullptr);
   for (int l = 0; l < Lv; ++l) C_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_c[std::size_t(l)]);
+  D_.assign(std::size_t(Lv) + 1, nullptr);
+  for (int l = 1; l < Lv; ++l) D_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_d[std::size_t(l)]);
   for (int l = 1; l <= Lv; ++l) Z_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_z[std::size_t(l)]);
   stage_[0] = reinterpret_cast<T*>(ws_ + off_s0);
   stage_[1] = reinterpret_cast<T*>(ws_ + off_s1);
@@ -317,16 +347,92 @@ void PlanT<T>::correction(int l, const T* in, T* z, T* apply, int sign, cudaStre
   }
 }
 
+// Thomas passes (thomas_pass, correction.hpp:335-339) on z over the real dims
+// in ascending order; the last pass writes last_out (which may equal z).
 template <class T>
-bool PlanT<T>::fused_ok(int) const {
-  return false;
+void PlanT<T>::thomas_all(int l, T* z, T* last_out, cudaStream_t s) {
+  const LevelArgs<T>& a = args_[std::size_t(l)];
+  const int64_t c[3] = {a.c[0], a.c[1], a.c[2]};
+  for (int k = 3 - h.rank; k < 3; ++k) {
+    T* dst = (k == 2) ? last_out : z;
+    ++launch_count_;
+    if (launch_thomas_fast<T>(z, dst, c, k, a.mult[k], a.rpiv[k], a.upper[k], s)) continue;
+    launch_thomas<T>(z, c, k, a.mult[k], a.rpiv[k], a.upper[k], nullptr, 0, s);
+    if (dst != z)
+      HGR_CUDA_CHECK(cudaMemcpyAsync(dst, z, std::size_t(c[0] * c[1] * c[2]) * sizeof(T),
+                                     cudaMemcpyDeviceToDevice, s));
+  }
 }
 
-// decompose (refactor.hpp:32-57) on the compact-level schedule:
-//   levels L..1: GPK (coefficients in place + gather of the coarse nodes into
-//   C_{l-1}), correction of the coefficients, C_{l-1} += z (fused into the last
-//   Thomas pass); then the pyramid is assembled by writing each C_{l-1} back to
-//   the even positions of level l.
+// One decompose level (refactor.hpp:41-54): coefficients of level l into
+// coef_dst and the corrected level-(l-1) nodal values into C_{l-1}.
+template <class T>
+void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, cudaStream_t s) {
+  const LevelArgs<T>& a = args_[std::size_t(l)];
+  T* Cn = C_[std::size_t(l) - 1];
+  T* z = Z_[std::size_t(l)];
+  const bool top = l == L();
+  if (big(l)) {
+    if (!in_place &&
+        launch_level_fused<T>(src, coef_dst, z, nullptr, a, kFusedDecompose, top ? d_flag_ : nullptr, s)) {
+      ++launch_count_;
+      thomas_all(l, z, Cn, s);  // C_{l-1} = M_c^-1 K U = coarse + z
+      return;
+    }
+    if (in_place &&
+        launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s)) {
+      launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);  // coefficients in place
+      launch_count_ += 2;
+      thomas_all(l, z, Cn, s);
+      return;
+    }
+  }
+  // reference-faithful small-level path: GPK, gather, correction of the
+  // coefficients, coarse += z (fused into the last Thomas pass)
+  if (in_place) {
+    launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);
+    ++launch_count_;
+  } else {
+    if (top) {
+      check_finite<T>(src, a.e[0] * a.e[1] * a.e[2], d_flag_, s);
+      ++launch_count_;
+    }
+    launch_coefficients<T>(src, coef_dst, a, s);
+    launch_gather<T>(src, a.e, 2, Cn, a.c, s);
+    launch_count_ += 2;
+  }
+  correction(l, coef_dst, z, Cn, +1, s);
+}
+
+// decompose (refactor.hpp:32-57) on compact level arrays: levels L..1 write the
+// level-l coefficients (level L into the output, coarser ones into D_l) and the
+// corrected coarse values C_{l-1}; the pyramid is then assembled bottom-up by
+// writing each finished level-(l-1) pyramid into the even positions of level l.
+template <class T>
+void PlanT<T>::decompose_to(const void* d_in, void* d_out, cudaStream_t s) {
+  if (d_in == d_out) return decompose(d_out, s);
+  const T* in = static_cast<const T*>(d_in);
+  T* out = static_cast<T*>(d_out);
+  launch_count_ = 0;
+  HGR_CUDA_CHECK(cudaMemsetAsync(d_flag_, 0, sizeof(int), s));
+  const int Lv = L();
+  if (Lv == 0) {
+    check_finite<T>(in, h.node_count(0), d_flag_, s);
+    HGR_CUDA_CHECK(cudaMemcpyAsync(out, in, h.node_count(0) * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    launch_count_ = 1;
+    last_launches_[0] = launch_count_;
+    return;
+  }
+  for (int l = Lv; l >= 1; --l)
+    decompose_level(l, l == Lv ? in : C_[std::size_t(l)], l == Lv ? out : D_[std::size_t(l)], false, s);
+  for (int l = 1; l <= Lv; ++l) {
+    launch_scatter_even<T>(l == 1 ? C_[0] : D_[std::size_t(l) - 1], l == Lv ? out : D_[std::size_t(l)],
+                           args_[std::size_t(l)], s);
+    ++launch_count_;
+  }
+  last_launches_[0] = launch_count_;
+}
+
 template <class T>
 void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
   T* data = static_cast<T*>(d_data);
@@ -335,25 +441,24 @@ void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
   const int Lv = L();
   if (Lv == 0) {
     check_finite<T>(data, h.node_count(0), d_flag_, s);
-    ++launch_count_;
+    launch_count_ = 1;
+    last_launches_[0] = launch_count_;
     return;
   }
-  auto level_ptr = [&](int l) { return l == Lv ? data : C_[std::size_t(l)]; };
-  for (int l = Lv; l >= 1; --l) {
-    launch_gpk_dec<T>(level_ptr(l), C_[std::size_t(l) - 1], args_[std::size_t(l)], d_flag_,
-                      l == Lv, s);
-    ++launch_count_;
-    correction(l, level_ptr(l), Z_[std::size_t(l)], C_[std::size_t(l) - 1], +1, s);
-  }
+  decompose_level(Lv, data, data, true, s);
+  for (int l = Lv - 1; l >= 1; --l) decompose_level(l, C_[std::size_t(l)], D_[std::size_t(l)], false, s);
   for (int l = 1; l <= Lv; ++l) {
-    launch_scatter_even<T>(C_[std::size_t(l) - 1], level_ptr(l), args_[std::size_t(l)], s);
+    launch_scatter_even<T>(l == 1 ? C_[0] : D_[std::size_t(l) - 1], l == Lv ? data : D_[std::size_t(l)],
+                           args_[std::size_t(l)], s);
     ++launch_count_;
   }
+  last_launches_[0] = launch_count_;
 }
 
-// recompose (refactor.hpp:63-90): corrections are computed top-down while the
-// coarse nodes are gathered into compact level arrays, then levels 1..L apply
-// coarse -= z and the interpolation (refined nodes = coef + interp).
+// recompose (refactor.hpp:63-90): top-down, each level's correction z_l is
+// computed from its coefficients (masked LPK + Thomas) while its coarse nodes
+// (the coarser pyramid) are gathered into C_{l-1}; bottom-up, each level
+// applies coarse -= z_l and the interpolation (refined = coef + interp).
 template <class T>
 void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
   const T* in = static_cast<const T*>(d_in);
@@ -365,6 +470,7 @@ void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
     if (out != in)
       HGR_CUDA_CHECK(cudaMemcpyAsync(out, in, h.node_count(0) * sizeof(T),
                                      cudaMemcpyDeviceToDevice, s));
+    last_launches_[1] = 0;
     return;
   }
   const auto& fe = ext_[std::size_t(Lv)];
@@ -375,6 +481,13 @@ void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
   }
   for (int l = m; l >= 1; --l) {
     const T* src = l == Lv ? in : C_[std::size_t(l)];
+    const LevelArgs<T>& a = args_[std::size_t(l)];
+    if (big(l) && launch_level_fused<T>(src, nullptr, Z_[std::size_t(l)], C_[std::size_t(l) - 1], a,
+                                        kFusedRecompose, nullptr, s)) {
+      ++launch_count_;
+      thomas_all(l, Z_[std::size_t(l)], Z_[std::size_t(l)], s);
+      continue;
+    }
     correction(l, src, Z_[std::size_t(l)], nullptr, 0, s);
     launch_gather<T>(src, ext_[std::size_t(l)].data(), 2, C_[std::size_t(l) - 1],
                      ext_[std::size_t(l) - 1].data(), s);
@@ -384,19 +497,18 @@ void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
     const bool with = l <= m;
     const T* coef = l == Lv ? in : C_[std::size_t(l)];
     T* dst = l == Lv ? out : C_[std::size_t(l)];
-    launch_gpk_rec<T>(coef, dst, C_[std::size_t(l) - 1], with ? Z_[std::size_t(l)] : nullptr,
-                      args_[std::size_t(l)], with, s);
+    const T* Z = with ? Z_[std::size_t(l)] : nullptr;
     ++launch_count_;
+    if (big(l) && launch_interp_rec<T>(coef, dst, C_[std::size_t(l) - 1], Z, args_[std::size_t(l)], with, s))
+      continue;
+    launch_gpk_rec<T>(coef, dst, C_[std::size_t(l) - 1], Z, args_[std::size_t(l)], with, s);
   }
+  last_launches_[1] = launch_count_;
 }
 
 template <class T>
-int PlanT<T>::launches(int direction, int upto) {
-  // dry count: mirrors the schedule above
-  const int Lv = L(), rank = h.rank;
-  if (direction == 0) return Lv == 0 ? 1 : Lv * (1 + 2 * rank) + Lv;
-  if (Lv == 0) return 0;
-  return (upto < Lv ? 1 : 0) + upto * (2 * rank + 1) + Lv;
+int PlanT<T>::launches(int direction, int) {
+  return last_launches_[direction ? 1 : 0];
 }
 
 template <class T>

@@ -58,6 +58,7 @@ class Plan {
   int dtype = HGR_F64;
   int device = 0;
   virtual void decompose(void* d_data, cudaStream_t s) = 0;
+  virtual void decompose_to(const void* d_in, void* d_out, cudaStream_t s) = 0;
   virtual void recompose(const void* d_in, void* d_out, int upto, cudaStream_t s) = 0;
   virtual int launches(int direction, int upto) = 0;
   virtual std::size_t workspace_bytes() const = 0;

@@ -192,3 +192,55 @@ def test_fiber_ops_vs_oracle(cuda, port, n):
     np.testing.assert_allclose(hgr.masstrans_apply(v, h), port.masstrans_apply(v, h), rtol=0, atol=1e-13)
     np.testing.assert_allclose(hgr.thomas_solve(v, h), port.thomas_solve(v, h), rtol=0, atol=1e-13)
     np.testing.assert_allclose(hgr.mass_apply(v, h), port.mass_apply(v, h), rtol=0, atol=1e-13)
+
+
+FUSED_SHAPES = [(65, 65, 65), (33, 129, 65), (129, 33, 17), (17, 257, 129), (257, 257), (1025, 65),
+                (65537,), (5, 65, 257), (9, 129, 33)]
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("nonuniform", [False, True], ids=["uniform", "nonuniform"])
+@pytest.mark.parametrize("shape", FUSED_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_fused_levels_vs_oracle(cuda, port, shape, nonuniform, dt):
+    """Sizes that take the fused level kernels (>= 2^15 nodes per level)."""
+    import torch
+    hgr = _hgr()
+    g, coords = make_grid(hgr, shape, nonuniform, seed=300)
+    from tests.synthetic import smooth_field
+    u = smooth_field(shape, dt, 12345)
+    scale = float(np.abs(u).max())
+    tol = TOL[dt]
+    expect = port.decompose(u, coords)
+    x = torch.from_numpy(u).to(cuda)
+    plan = hgr.Plan(g, "f64" if dt == np.float64 else "f32")
+    out = torch.empty_like(x)
+    plan.decompose_into(x, out)
+    plan.sync_status()
+    assert torch.equal(x, torch.from_numpy(u).to(cuda)), "decompose_into must not modify its input"
+    assert rel(out.cpu().numpy(), expect, scale) <= tol
+    inplace = x.clone()
+    plan.decompose_(inplace)
+    plan.sync_status()
+    assert rel(inplace.cpu().numpy(), expect, scale) <= tol
+    L = g.levels()
+    for m in sorted({0, L - 1, L}):
+        back = torch.empty_like(x)
+        plan.recompose_into(out, back, m)
+        assert rel(back.cpu().numpy(), port.recompose(expect, m, coords), scale) <= tol, m
+    same = out.clone()
+    plan.recompose_into(same, same, L)  # in-place recompose
+    assert rel(same.cpu().numpy(), u, scale) <= tol
+
+
+def test_nonfinite_fused(cuda):
+    import torch
+    hgr = _hgr()
+    g = hgr.GridHierarchy.uniform([33, 33, 33])
+    x = torch.rand(33, 33, 33, dtype=torch.float64, device=cuda)
+    x[17, 5, 30] = float("inf")
+    with pytest.raises(hgr.HgrError, match="non-finite"):
+        hgr.decompose(x, g)
+    plan = hgr.Plan(g, "f64")
+    plan.decompose_(x)
+    with pytest.raises(hgr.HgrError, match="non-finite"):
+        plan.sync_status()
