@@ -85,6 +85,28 @@ int hgr_cuda_plan_recompose(hgr_plan plan, const void* d_in, void* d_out, int up
 /* synchronizes `stream`; returns HGR_ERR_NONFINITE if the last decompose saw NaN/Inf */
 int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream);
 
+/* Per-launch profile (no reference counterpart; bench/roofline support). When
+ * enabled, every launch of the plan is bracketed by CUDA events on its stream
+ * and charged to a kernel class with its algorithmic bytes. Classes:
+ * 0 fused decompose level, 1 fused recompose level, 2 Thomas passes,
+ * 3 recompose interpolation, 4 assembly/gathers, 5 small-level kernels.
+ * read_profile synchronizes and returns the totals since set_profiling. */
+#define HGR_KIND_COUNT 6
+int hgr_cuda_plan_set_profiling(hgr_plan plan, int enable);
+int hgr_cuda_plan_read_profile(hgr_plan plan, double* ms, double* bytes, long* launches);
+
+/* Synthetic input (bench/test data): u = a[i]*b[j] + c[k] +
+ * 1e-3*eta(seed + flat) with eta from splitmix64 in [-1, 1), computed in
+ * double with IEEE-exact mul/add and rounded once to the dtype. The factor
+ * tables (host, lengths = extents padded to rank 3 on the right) are supplied
+ * by the caller so host and device fields are bitwise identical. */
+int hgr_cuda_synthetic_field_f64(const hgr_grid_desc* g, double* d_out, unsigned long long seed,
+                                 const double* h_a, const double* h_b, const double* h_c,
+                                 void* stream);
+int hgr_cuda_synthetic_field_f32(const hgr_grid_desc* g, float* d_out, unsigned long long seed,
+                                 const double* h_a, const double* h_b, const double* h_c,
+                                 void* stream);
+
 /* ---- one-shot entry points (plan cached by grid + dtype) --------------------
  * C-ABI twins of hgr::decompose<T> / hgr::recompose<T> (refactor.hpp:32-33, :63-64). */
 int hgr_cuda_decompose_f64(const hgr_grid_desc* grid, double* d_data, void* stream);

@@ -235,6 +235,20 @@ class Plan:
     def sync_status(self, stream: Optional[int] = None) -> None:
         _check(_lib.load().hgr_cuda_plan_sync_status(self._h, stream))
 
+    KINDS = ("fused_decompose_level", "fused_recompose_level", "thomas", "recompose_interp",
+             "assembly", "small_levels")
+
+    def set_profiling(self, on: bool) -> None:
+        """Bracket every launch with CUDA events (per kernel class); resets totals."""
+        _check(_lib.load().hgr_cuda_plan_set_profiling(self._h, 1 if on else 0))
+
+    def read_profile(self) -> dict:
+        """{kind: (ms, algorithmic bytes, launches)} since set_profiling (synchronizes)."""
+        n = len(self.KINDS)
+        ms, by, la = (C.c_double * n)(), (C.c_double * n)(), (C.c_long * n)()
+        _check(_lib.load().hgr_cuda_plan_read_profile(self._h, ms, by, la))
+        return {k: (ms[i], by[i], la[i]) for i, k in enumerate(self.KINDS)}
+
 
 def _check_shape(data, g: GridHierarchy, what: str) -> None:
     if list(data.shape) != g.finest_extents():
@@ -405,6 +419,29 @@ def _fiber(op: str, v, h, nout_fn):
     _check(getattr(_lib.load(), f"hgr_cuda_{op}_{_dtype_tag(d)}")(
         n, count, _ptr(d), hh.ctypes.data, _ptr(out), _stream_of(d)))
     return _back(out, was)
+
+
+def synthetic_field(shape, dtype: str = "f64", seed: int = 12345, device=None):
+    """Deterministic benchmark field on the device:
+    sin(0.21 i) cos(0.13 j) + 0.5 sin(0.07 k) + 1e-3 eta(seed + flat), bitwise
+    identical to tests/synthetic.smooth_field (factor tables built here with
+    numpy, combined on the device with IEEE-exact mul/add)."""
+    import torch
+    e = list(shape) + [1] * (3 - len(shape))
+    i, j, k = (np.arange(n, dtype=np.float64) for n in e)
+    fa = np.ascontiguousarray(np.sin(0.21 * i))
+    fb = np.ascontiguousarray(np.cos(0.13 * j))
+    fc = np.ascontiguousarray(0.5 * np.sin(0.07 * k))
+    out = torch.empty(tuple(shape), dtype=torch.float64 if dtype == "f64" else torch.float32,
+                      device=device or "cuda")
+    desc = _lib.GridDesc()
+    desc.rank = len(shape)
+    for d, n in enumerate(shape):
+        desc.extents[d] = n
+    _check(getattr(_lib.load(), f"hgr_cuda_synthetic_field_{dtype}")(
+        C.byref(desc), _ptr(out), C.c_ulonglong(seed), fa.ctypes.data, fb.ctypes.data,
+        fc.ctypes.data, _stream_of(out)))
+    return out
 
 
 def mass_apply(v, h):

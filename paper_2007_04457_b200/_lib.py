@@ -34,6 +34,10 @@ _SIGS = {
     "hgr_cuda_plan_decompose_to": (_int, [_vp, _vp, _vp, _vp]),
     "hgr_cuda_plan_recompose": (_int, [_vp, _vp, _vp, _int, _vp]),
     "hgr_cuda_plan_sync_status": (_int, [_vp, _vp]),
+    "hgr_cuda_plan_set_profiling": (_int, [_vp, _int]),
+    "hgr_cuda_plan_read_profile": (_int, [_vp, _vp, _vp, _vp]),
+    "hgr_cuda_synthetic_field_f64": (_int, [_G, _vp, C.c_ulonglong, _vp, _vp, _vp, _vp]),
+    "hgr_cuda_synthetic_field_f32": (_int, [_G, _vp, C.c_ulonglong, _vp, _vp, _vp, _vp]),
     "hgr_class_node_count": (_sz, [_G, _int]),
     "hgr_levels": (_int, [_G]),
 }

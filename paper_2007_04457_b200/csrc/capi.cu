@@ -327,6 +327,35 @@ int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream) {
   return rc;
 }
 
+int hgr_cuda_plan_set_profiling(hgr_plan plan, int enable) {
+  return guarded([&] {
+    hgrb::require(plan != nullptr, "plan is null");
+    plan->plan->set_profiling(enable != 0);
+  });
+}
+
+int hgr_cuda_plan_read_profile(hgr_plan plan, double* ms, double* bytes, long* launches) {
+  return guarded([&] {
+    hgrb::require(plan != nullptr, "plan is null");
+    hgrb::KindStats st[hgrb::kKindCount];
+    plan->plan->read_profile(st);
+    for (int i = 0; i < hgrb::kKindCount; ++i) {
+      if (ms) ms[i] = st[i].ms;
+      if (bytes) bytes[i] = st[i].bytes;
+      if (launches) launches[i] = st[i].launches;
+    }
+  });
+}
+
+int hgr_cuda_synthetic_field_f64(const hgr_grid_desc* g, double* d, unsigned long long seed,
+                                 const double* a, const double* b, const double* c, void* s) {
+  return guarded([&] { hgrb::synthetic_field<double>(g, d, seed, a, b, c, as_stream(s)); });
+}
+int hgr_cuda_synthetic_field_f32(const hgr_grid_desc* g, float* d, unsigned long long seed,
+                                 const double* a, const double* b, const double* c, void* s) {
+  return guarded([&] { hgrb::synthetic_field<float>(g, d, seed, a, b, c, as_stream(s)); });
+}
+
 int hgr_cuda_decompose_f64(const hgr_grid_desc* g, double* d, void* s) { return decompose_dev(g, d, s); }
 int hgr_cuda_decompose_f32(const hgr_grid_desc* g, float* d, void* s) { return decompose_dev(g, d, s); }
 int hgr_cuda_decompose_to_f64(const hgr_grid_desc* g, const double* i, double* o, void* s) {

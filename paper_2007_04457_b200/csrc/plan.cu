@@ -71,6 +71,60 @@ int Plan::sync_status(cudaStream_t s) {
   return *h_flag_ ? HGR_ERR_NONFINITE : HGR_OK;
 }
 
+Plan::~Plan() {
+  for (auto& r : prof_pending_) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : ev_free_) cudaEventDestroy(e);
+}
+
+cudaEvent_t Plan::take_event() {
+  if (!ev_free_.empty()) {
+    cudaEvent_t e = ev_free_.back();
+    ev_free_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  HGR_CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+
+void Plan::set_profiling(bool on) {
+  KindStats drop[kKindCount];
+  read_profile(drop);  // recycles pending events
+  for (auto& k : prof_acc_) k = KindStats{};
+  profiling_ = on;
+}
+
+void Plan::prof_begin(int kind, double bytes, cudaStream_t s) {
+  if (!profiling_) return;
+  ProfRec r{kind, bytes, take_event(), take_event()};
+  HGR_CUDA_CHECK(cudaEventRecord(r.a, s));
+  prof_pending_.push_back(r);
+}
+
+void Plan::prof_end(cudaStream_t s) {
+  if (!profiling_) return;
+  HGR_CUDA_CHECK(cudaEventRecord(prof_pending_.back().b, s));
+}
+
+void Plan::read_profile(KindStats out[kKindCount]) {
+  for (auto& r : prof_pending_) {
+    HGR_CUDA_CHECK(cudaEventSynchronize(r.b));
+    float ms = 0;
+    HGR_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    KindStats& k = prof_acc_[r.kind];
+    k.ms += ms;
+    k.bytes += r.bytes;
+    k.launches += 1;
+    ev_free_.push_back(r.a);
+    ev_free_.push_back(r.b);
+  }
+  prof_pending_.clear();
+  for (int i = 0; i < kKindCount; ++i) out[i] = prof_acc_[i];
+}
+
 // ---- precision-specific plan ----------------------------------------------------
 
 namespace {
@@ -162,6 +216,8 @@ class PlanT final : public Plan {
  private:
   void correction(int l, const T* in, T* z, T* apply, int sign, cudaStream_t s);
   void thomas_all(int l, T* z, T* last_out, cudaStream_t s);
+  void assemble(T* out, cudaStream_t s);
+  static constexpr double sz() { return double(sizeof(T)); }
   void decompose_level(int l, const T* src, T* coef_dst, bool in_place, cudaStream_t s);
   bool big(int l) const { return h.node_count(l) >= (std::size_t(1) << 15); }
   int L() const { return h.L; }
@@ -335,14 +391,19 @@ void PlanT<T>::correction(int l, const T* in, T* z, T* apply, int sign, cudaStre
   int pass = 0;
   for (int k = 3 - rank; k < 3; ++k, ++pass) {
     T* dst = (k == 2) ? z : stage_[pass & 1];
+    const double n_in = double(e[0] * e[1] * e[2]);
+    prof_begin(kKindSmall, sz() * (n_in + n_in / double(e[k]) * double(a.c[k])), s);
     launch_lpk<T>(cur, e, dst, k, a.c[k], a.taps[k], pass == 0, s);
+    prof_end(s);
     ++launch_count_;
     e[k] = a.c[k];
     cur = dst;
   }
   for (int k = 3 - rank; k < 3; ++k) {
     const bool last = k == 2;
+    prof_begin(kKindThomas, sz() * 2.0 * double(e[0] * e[1] * e[2]), s);
     launch_thomas<T>(z, e, k, a.mult[k], a.rpiv[k], a.upper[k], last ? apply : nullptr, sign, s);
+    prof_end(s);
     ++launch_count_;
   }
 }
@@ -356,11 +417,15 @@ void PlanT<T>::thomas_all(int l, T* z, T* last_out, cudaStream_t s) {
   for (int k = 3 - h.rank; k < 3; ++k) {
     T* dst = (k == 2) ? last_out : z;
     ++launch_count_;
-    if (launch_thomas_fast<T>(z, dst, c, k, a.mult[k], a.rpiv[k], a.upper[k], s)) continue;
-    launch_thomas<T>(z, c, k, a.mult[k], a.rpiv[k], a.upper[k], nullptr, 0, s);
-    if (dst != z)
-      HGR_CUDA_CHECK(cudaMemcpyAsync(dst, z, std::size_t(c[0] * c[1] * c[2]) * sizeof(T),
-                                     cudaMemcpyDeviceToDevice, s));
+    prof_begin(kKindThomas, sz() * 2.0 * double(c[0] * c[1] * c[2]), s);
+    const bool fast = launch_thomas_fast<T>(z, dst, c, k, a.mult[k], a.rpiv[k], a.upper[k], s);
+    if (!fast) {
+      launch_thomas<T>(z, c, k, a.mult[k], a.rpiv[k], a.upper[k], nullptr, 0, s);
+      if (dst != z)
+        HGR_CUDA_CHECK(cudaMemcpyAsync(dst, z, std::size_t(c[0] * c[1] * c[2]) * sizeof(T),
+                                       cudaMemcpyDeviceToDevice, s));
+    }
+    prof_end(s);
   }
 }
 
@@ -372,23 +437,36 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
   T* Cn = C_[std::size_t(l) - 1];
   T* z = Z_[std::size_t(l)];
   const bool top = l == L();
+  const double n = double(h.node_count(l)), c = double(h.node_count(l - 1));
   if (big(l)) {
-    if (!in_place &&
-        launch_level_fused<T>(src, coef_dst, z, nullptr, a, kFusedDecompose, top ? d_flag_ : nullptr, s)) {
-      ++launch_count_;
-      thomas_all(l, z, Cn, s);  // C_{l-1} = M_c^-1 K U = coarse + z
-      return;
-    }
-    if (in_place &&
-        launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s)) {
-      launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);  // coefficients in place
-      launch_count_ += 2;
-      thomas_all(l, z, Cn, s);
-      return;
+    if (!in_place) {
+      // read the level once, write the coefficients and the load vector once
+      prof_begin(kKindFusedDec, sz() * (n + (n - c) + c), s);
+      const bool ok = launch_level_fused<T>(src, coef_dst, z, nullptr, a, kFusedDecompose,
+                                            top ? d_flag_ : nullptr, s);
+      prof_end(s);
+      if (ok) {
+        ++launch_count_;
+        thomas_all(l, z, Cn, s);  // C_{l-1} = M_c^-1 K U = coarse + z
+        return;
+      }
+    } else {
+      prof_begin(kKindFusedDec, sz() * (n + c), s);
+      const bool ok = launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s);
+      prof_end(s);
+      if (ok) {
+        prof_begin(kKindSmall, sz() * (n + (n - c)), s);
+        launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);  // coefficients in place
+        prof_end(s);
+        launch_count_ += 2;
+        thomas_all(l, z, Cn, s);
+        return;
+      }
     }
   }
   // reference-faithful small-level path: GPK, gather, correction of the
   // coefficients, coarse += z (fused into the last Thomas pass)
+  prof_begin(kKindSmall, sz() * (2 * n + c), s);
   if (in_place) {
     launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);
     ++launch_count_;
@@ -401,7 +479,22 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
     launch_gather<T>(src, a.e, 2, Cn, a.c, s);
     launch_count_ += 2;
   }
+  prof_end(s);
   correction(l, coef_dst, z, Cn, +1, s);
+}
+
+// pyramid assembly: each finished level-(l-1) pyramid into the even positions
+// of level l (C_0 -> D_1 -> ... -> D_{L-1} -> out)
+template <class T>
+void PlanT<T>::assemble(T* out, cudaStream_t s) {
+  const int Lv = L();
+  for (int l = 1; l <= Lv; ++l) {
+    prof_begin(kKindAssembly, sz() * 2.0 * double(h.node_count(l - 1)), s);
+    launch_scatter_even<T>(l == 1 ? C_[0] : D_[std::size_t(l) - 1], l == Lv ? out : D_[std::size_t(l)],
+                           args_[std::size_t(l)], s);
+    prof_end(s);
+    ++launch_count_;
+  }
 }
 
 // decompose (refactor.hpp:32-57) on compact level arrays: levels L..1 write the
@@ -425,11 +518,7 @@ void PlanT<T>::decompose_to(const void* d_in, void* d_out, cudaStream_t s) {
   }
   for (int l = Lv; l >= 1; --l)
     decompose_level(l, l == Lv ? in : C_[std::size_t(l)], l == Lv ? out : D_[std::size_t(l)], false, s);
-  for (int l = 1; l <= Lv; ++l) {
-    launch_scatter_even<T>(l == 1 ? C_[0] : D_[std::size_t(l) - 1], l == Lv ? out : D_[std::size_t(l)],
-                           args_[std::size_t(l)], s);
-    ++launch_count_;
-  }
+  assemble(out, s);
   last_launches_[0] = launch_count_;
 }
 
@@ -447,11 +536,7 @@ void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
   }
   decompose_level(Lv, data, data, true, s);
   for (int l = Lv - 1; l >= 1; --l) decompose_level(l, C_[std::size_t(l)], D_[std::size_t(l)], false, s);
-  for (int l = 1; l <= Lv; ++l) {
-    launch_scatter_even<T>(l == 1 ? C_[0] : D_[std::size_t(l) - 1], l == Lv ? data : D_[std::size_t(l)],
-                           args_[std::size_t(l)], s);
-    ++launch_count_;
-  }
+  assemble(data, s);
   last_launches_[0] = launch_count_;
 }
 
@@ -475,22 +560,33 @@ void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
   }
   const auto& fe = ext_[std::size_t(Lv)];
   if (m < Lv) {
+    prof_begin(kKindAssembly, sz() * 2.0 * double(h.node_count(m)), s);
     launch_gather<T>(in, fe.data(), int64_t(1) << (Lv - m), C_[std::size_t(m)],
                      ext_[std::size_t(m)].data(), s);
+    prof_end(s);
     ++launch_count_;
   }
   for (int l = m; l >= 1; --l) {
     const T* src = l == Lv ? in : C_[std::size_t(l)];
     const LevelArgs<T>& a = args_[std::size_t(l)];
-    if (big(l) && launch_level_fused<T>(src, nullptr, Z_[std::size_t(l)], C_[std::size_t(l) - 1], a,
-                                        kFusedRecompose, nullptr, s)) {
-      ++launch_count_;
-      thomas_all(l, Z_[std::size_t(l)], Z_[std::size_t(l)], s);
-      continue;
+    const double n = double(h.node_count(l)), c = double(h.node_count(l - 1));
+    if (big(l)) {
+      // read the level once, write the load vector and the gathered coarse nodes
+      prof_begin(kKindFusedRec, sz() * (n + 2 * c), s);
+      const bool ok = launch_level_fused<T>(src, nullptr, Z_[std::size_t(l)],
+                                            C_[std::size_t(l) - 1], a, kFusedRecompose, nullptr, s);
+      prof_end(s);
+      if (ok) {
+        ++launch_count_;
+        thomas_all(l, Z_[std::size_t(l)], Z_[std::size_t(l)], s);
+        continue;
+      }
     }
     correction(l, src, Z_[std::size_t(l)], nullptr, 0, s);
+    prof_begin(kKindSmall, sz() * 2.0 * c, s);
     launch_gather<T>(src, ext_[std::size_t(l)].data(), 2, C_[std::size_t(l) - 1],
                      ext_[std::size_t(l) - 1].data(), s);
+    prof_end(s);
     ++launch_count_;
   }
   for (int l = 1; l <= Lv; ++l) {
@@ -498,10 +594,20 @@ void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
     const T* coef = l == Lv ? in : C_[std::size_t(l)];
     T* dst = l == Lv ? out : C_[std::size_t(l)];
     const T* Z = with ? Z_[std::size_t(l)] : nullptr;
+    const double n = double(h.node_count(l)), c = double(h.node_count(l - 1));
     ++launch_count_;
-    if (big(l) && launch_interp_rec<T>(coef, dst, C_[std::size_t(l) - 1], Z, args_[std::size_t(l)], with, s))
-      continue;
+    // read the coefficients (if any) and the coarse block (C, Z), write the level
+    const double bytes = sz() * ((with ? (n - c) + 2 * c : c) + n);
+    if (big(l)) {
+      prof_begin(kKindInterp, bytes, s);
+      const bool ok = launch_interp_rec<T>(coef, dst, C_[std::size_t(l) - 1], Z,
+                                           args_[std::size_t(l)], with, s);
+      prof_end(s);
+      if (ok) continue;
+    }
+    prof_begin(kKindSmall, bytes, s);
     launch_gpk_rec<T>(coef, dst, C_[std::size_t(l) - 1], Z, args_[std::size_t(l)], with, s);
+    prof_end(s);
   }
   last_launches_[1] = launch_count_;
 }

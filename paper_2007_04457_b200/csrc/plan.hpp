@@ -46,17 +46,34 @@ struct Hierarchy {
   void canon_extents(int l, int64_t e[3]) const;
 };
 
-// Kernel launch accounting (for bench's gpu_launches and the plan API).
-struct LaunchCounter {
-  int count = 0;
+// Kernel classes for the optional per-launch CUDA-event profile (bench.py's
+// roofline of the dominant kernel). Order matches HGR_KIND_* in hgr_cuda.h.
+enum KernelKind : int {
+  kKindFusedDec = 0,   // k_level_fused, decompose (GPK + LPK)
+  kKindFusedRec = 1,   // k_level_fused, recompose (masked LPK + gather)
+  kKindThomas = 2,     // IPK passes
+  kKindInterp = 3,     // recompose interpolation (GPK^-1)
+  kKindAssembly = 4,   // pyramid assembly / gathers
+  kKindSmall = 5,      // one-thread-per-item kernels of the small levels
+  kKindCount = 6
+};
+
+struct KindStats {
+  double ms = 0, bytes = 0;
+  long launches = 0;
 };
 
 class Plan {
  public:
-  virtual ~Plan() = default;
+  virtual ~Plan();
   Hierarchy h;
   int dtype = HGR_F64;
   int device = 0;
+
+  // profiling: when enabled, every launch is bracketed by CUDA events on its
+  // stream and charged to its kernel class with its algorithmic bytes
+  void set_profiling(bool on);
+  void read_profile(KindStats out[kKindCount]);  // synchronizes; clears the window
   virtual void decompose(void* d_data, cudaStream_t s) = 0;
   virtual void decompose_to(const void* d_in, void* d_out, cudaStream_t s) = 0;
   virtual void recompose(const void* d_in, void* d_out, int upto, cudaStream_t s) = 0;
@@ -73,8 +90,27 @@ class Plan {
  protected:
   int* d_flag_ = nullptr;   // non-finite flag set by the level-L decompose kernel
   int* h_flag_ = nullptr;   // pinned mirror
+
+  // profiling helpers (no-ops unless enabled)
+  void prof_begin(int kind, double bytes, cudaStream_t s);
+  void prof_end(cudaStream_t s);
+  struct ProfRec {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  bool profiling_ = false;
+  std::vector<ProfRec> prof_pending_;
+  std::vector<cudaEvent_t> ev_free_;
+  KindStats prof_acc_[kKindCount];
+  cudaEvent_t take_event();
 };
 
 std::unique_ptr<Plan> make_plan(const hgr_grid_desc* g, int dtype);
+
+// synth.cu
+template <class T>
+void synthetic_field(const hgr_grid_desc* g, T* out, uint64_t seed, const double* ha,
+                     const double* hb, const double* hc, cudaStream_t s);
 
 }  // namespace hgrb
