@@ -146,6 +146,25 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+def shard_seed(rank):
+    """Each rank refactors its own independent block: seed 12345 + rank."""
+    return 12345 + rank
+
+
+def reduce_across_ranks(ms_step, checksum, device=None):
+    """The only collectives of a multi-GPU run, after the timed region: max of
+    the per-rank step time and sum of the per-block checksums.
+    Works with NCCL (GPU tensors) or gloo (CPU tensors, tests)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms_step)], dtype=torch.float64, device=device)
+    c = torch.tensor([float(checksum)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(c.item())
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -247,7 +266,7 @@ def run_gpu(args, cfg):
     g = hgr.GridHierarchy(coords) if coords else hgr.GridHierarchy.uniform(list(shape))
     L = g.levels()
     plan = hgr.Plan(g, dt)
-    x = hgr.synthetic_field(shape, dt, seed=12345 + rank, device=dev)
+    x = hgr.synthetic_field(shape, dt, seed=shard_seed(rank), device=dev)
     x0 = x.clone()
     P = torch.empty_like(x)
     S = x.element_size()
@@ -289,12 +308,7 @@ def run_gpu(args, cfg):
     plan.set_profiling(False)
     launches_step = plan.launches(0, L) + plan.launches(1, L)
 
-    t = torch.tensor([ms_step], dtype=torch.float64, device=dev)
-    chk = torch.tensor([float(x.double().sum().item())], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(chk, op=dist.ReduceOp.SUM)
-    ms_max = float(t.item())
+    ms_max, chk_sum = reduce_across_ranks(ms_step, float(x.double().sum().item()), dev)
     value = world * 2 * nbytes / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API: pinned host field -> device, full
@@ -316,10 +330,7 @@ def run_gpu(args, cfg):
         err_h = err_d.to("cpu", non_blocking=False)
     eb.record(stream)
     torch.cuda.synchronize(dev)
-    te = torch.tensor([ea.elapsed_time(eb) / e2e_steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+    e2e_ms, _ = reduce_across_ranks(ea.elapsed_time(eb) / e2e_steps, 0.0, dev)
     e2e_value = world * 2 * nbytes / (e2e_ms * 1e-3) / 1e9
     del host, xin, yout
 
@@ -366,7 +377,7 @@ def run_gpu(args, cfg):
         "gpu_launches": launches_step * args.steps,
         "clocks": clocks,
         "roundtrip_rel_err": rt_err,
-        "checksum": float(chk.item()),
+        "checksum": chk_sum,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_run(cfg, seconds_budget=args.cpu_seconds)

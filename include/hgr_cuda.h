@@ -149,6 +149,20 @@ int hgr_cuda_compute_correction_f64(const hgr_grid_desc* g, int level, const dou
 int hgr_cuda_compute_correction_f32(const hgr_grid_desc* g, int level, const float* d_coeffs,
                                     float* d_z, void* stream);
 
+/* Host-pointer twins of the single-level entry points (synchronous), used by
+ * the C++ drop-in: op 0 = interpolate_to_fine, 1 = compute_coefficients,
+ * 2 = compute_correction. h_in / h_out are compact level arrays. */
+int hgr_host_level_op_f64(const hgr_grid_desc* g, int op, int level, const double* h_in,
+                          double* h_out);
+int hgr_host_level_op_f32(const hgr_grid_desc* g, int op, int level, const float* h_in,
+                          float* h_out);
+/* Host-pointer fiber operators: op 0 = mass_apply, 1 = masstrans_apply,
+ * 2 = thomas_solve (correction.hpp:58-223); count fibers of length n. */
+int hgr_host_fiber_op_f64(int op, size_t n, size_t count, const double* h_v, const double* h_h,
+                          double* h_out);
+int hgr_host_fiber_op_f32(int op, size_t n, size_t count, const float* h_v, const float* h_h,
+                          float* h_out);
+
 /* ---- class packing (refactor.hpp:134-170) ----------------------------------
  * extract_class / scatter_class on the finest-shape pyramid, device pointers.
  * d_values holds class_node_count(cls) values in the reference's row-major order. */

@@ -262,9 +262,54 @@ int fiber_op(int op, std::size_t n, std::size_t count, const T* v, const T* h, T
   });
 }
 
+template <class T>
+int host_level_op(const hgr_grid_desc* g, int op, int level, const T* h_in, T* h_out) {
+  return guarded([&] {
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    hgrb::require(level >= 1 && level <= p->h.L, "level out of range");
+    const std::size_t nf = p->h.node_count(level), nc = p->h.node_count(level - 1);
+    const std::size_t nin = op == 0 ? nc : nf, nout = op == 2 ? nc : nf;
+    DevBuf<T> din(nin), dout(nout);
+    HGR_CUDA_CHECK(cudaMemcpy(din.p, h_in, nin * sizeof(T), cudaMemcpyHostToDevice));
+    cudaStream_t s = nullptr;
+    if (op == 0) p->interpolate_to_fine(level, din.p, dout.p, s);
+    else if (op == 1) p->compute_coefficients(level, din.p, dout.p, s);
+    else p->compute_correction(level, din.p, dout.p, s);
+    HGR_CUDA_CHECK(cudaMemcpy(h_out, dout.p, nout * sizeof(T), cudaMemcpyDeviceToHost));
+  });
+}
+
+template <class T>
+int host_fiber_op(int op, std::size_t n, std::size_t count, const T* h_v, const T* h_h, T* h_out) {
+  const std::size_t nout = op == 1 ? (n - 1) / 2 + 1 : n;
+  int rc = HGR_OK;
+  rc = guarded([&] {
+    hgrb::require(n >= 2, "mass matrix needs at least one interval");
+    DevBuf<T> dv(n * count), dout(nout * count);
+    HGR_CUDA_CHECK(cudaMemcpy(dv.p, h_v, n * count * sizeof(T), cudaMemcpyHostToDevice));
+    int r = fiber_op<T>(op, n, count, dv.p, h_h, dout.p, nullptr);
+    if (r != HGR_OK) throw Error(r, g_last_error);
+    HGR_CUDA_CHECK(cudaMemcpy(h_out, dout.p, nout * count * sizeof(T), cudaMemcpyDeviceToHost));
+  });
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
+
+int hgr_host_level_op_f64(const hgr_grid_desc* g, int op, int level, const double* i, double* o) {
+  return host_level_op(g, op, level, i, o);
+}
+int hgr_host_level_op_f32(const hgr_grid_desc* g, int op, int level, const float* i, float* o) {
+  return host_level_op(g, op, level, i, o);
+}
+int hgr_host_fiber_op_f64(int op, size_t n, size_t c, const double* v, const double* h, double* o) {
+  return host_fiber_op(op, n, c, v, h, o);
+}
+int hgr_host_fiber_op_f32(int op, size_t n, size_t c, const float* v, const float* h, float* o) {
+  return host_fiber_op(op, n, c, v, h, o);
+}
 
 const char* hgr_cuda_last_error(void) { return g_last_error.c_str(); }
 int hgr_cuda_abi_version(void) { return HGR_CUDA_ABI_VERSION; }

@@ -244,3 +244,32 @@ def test_nonfinite_fused(cuda):
     plan.decompose_(x)
     with pytest.raises(hgr.HgrError, match="non-finite"):
         plan.sync_status()
+
+
+@pytest.mark.parametrize("shape", [(33, 17, 9), (65, 129), (257,)], ids=str)
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_device_synthetic_field_bitwise(cuda, shape, dt):
+    """bench.py's device field == tests/synthetic.smooth_field, bit for bit."""
+    hgr = _hgr()
+    from tests.synthetic import smooth_field
+    dev = hgr.synthetic_field(shape, dt, seed=12345, device=cuda).cpu().numpy()
+    host = smooth_field(shape, np.float64 if dt == "f64" else np.float32, 12345)
+    assert np.array_equal(dev, host)
+
+
+@pytest.mark.parametrize("shape", [(65, 65, 65), (129, 65, 33)], ids=str)
+def test_profiled_run_matches_unprofiled(cuda, shape):
+    """The per-launch event profile (bench roofline) does not change results."""
+    import torch
+    hgr = _hgr()
+    g = hgr.GridHierarchy.uniform(list(shape))
+    x = hgr.synthetic_field(shape, "f64", device=cuda)
+    plan = hgr.Plan(g, "f64")
+    a, b = torch.empty_like(x), torch.empty_like(x)
+    plan.decompose_into(x, a)
+    plan.set_profiling(True)
+    plan.decompose_into(x, b)
+    prof = plan.read_profile()
+    plan.set_profiling(False)
+    assert torch.equal(a, b)
+    assert prof["fused_decompose_level"][2] >= 1 and prof["thomas"][2] >= 3
