@@ -3,11 +3,14 @@
 //
 //   A CTA (16 warps) owns a (dim1, dim2) tile of coarse outputs and marches
 //   along dim 0 over a segment of coarse planes. Each fine plane's halo window
-//   arrives in shared memory via 16-byte cp.async (LDGSTS) issued by all warps
-//   into an NS-slot mbarrier ring, two planes ahead. (Row copies through the
-//   TMA bulk engine were tried first: with ~500-byte rows the per-copy cost
-//   capped reads near 0.9 TB/s; tensor maps are unusable because 2^k+1 row
-//   pitches are not 16-byte multiples.)
+//   arrives in shared memory through 1D TMA tensor copies (one per window row,
+//   issued by lane 0 of every warp) into an NS-slot mbarrier ring, two planes
+//   ahead. A TMA box must start 16-byte aligned, and 2^k+1 row pitches make
+//   every row's phase differ, so each row lands as its aligned superset and the
+//   consumer offsets by the row's phase. (Measured on B200 with a streaming
+//   probe, tools/mb/stream_mb.cu: warp-issued 1D TMA rows move 6.9 TB/s of
+//   unique data, 16-byte cp.async by all threads 3.4 TB/s, one issuing thread
+//   1.8 TB/s.)
 //   Each warp owns a band of 4 window rows, lanes own window columns; what a
 //   lane needs about its columns (mass stencil row, interpolation weights,
 //   ownership) is computed once per CTA and kept in registers. Slots are zeroed
@@ -37,6 +40,7 @@
 #include "kernels_fused.cuh"
 #include "plan.hpp"
 #include "ptx.cuh"
+#include "tma.hpp"
 
 namespace hgrb {
 
@@ -44,10 +48,11 @@ namespace {
 
 // Tile shapes: 4 window rows per warp; 64 (fp64) or 128 (fp32) window columns,
 // except fp32 decompose, whose per-lane interpolant registers need the
-// narrower tile to stay spill-free.
+// narrower tile to stay spill-free. fp32 recompose uses 57 coarse columns so
+// the TMA box (the row's 16-byte aligned superset) fits a 128-float pitch.
 template <class T, int MODE>
 struct FCfg {
-  static constexpr int TW1 = 29, TW2 = (sizeof(T) == 4 && MODE != kFusedDecompose) ? 61 : 29;
+  static constexpr int TW1 = 29, TW2 = (sizeof(T) == 4 && MODE != kFusedDecompose) ? 57 : 29;
   static constexpr int NS = 5;
 };
 
@@ -57,7 +62,6 @@ template <class T, int TW1, int TW2, int NS>
 struct FLayout {
   static constexpr int NT = 512, NW = NT / 32;
   static constexpr int V = 16 / int(sizeof(T));
-  static constexpr int LOGV = V == 2 ? 1 : 2;
   static constexpr int RW = 2 * (TW1 + 1) + 3;        // max window rows
   static constexpr int CW = 2 * (TW2 + 1) + 3;        // max window cols
   static constexpr int KC = (CW + 31) / 32;           // column iterations per lane
@@ -67,11 +71,14 @@ struct FLayout {
   static constexpr int RC = (RW + NW - 1) / NW;       // rows a warp copies
   static constexpr int SQ = (TW1 + 1 + NW - 1) / NW;  // output rows per warp
   static constexpr int MW = KC * 32;                  // row pitch of the m buffer
-  // copies land at position 2V (room for the c-1 neighbour of window col 0 and
-  // the alignment shift); reads reach position row_off + MW <= 3V + MW
-  static constexpr int PITCH =
-      ((CW + 4 * V > MW + 3 * V + 1 ? CW + 4 * V : MW + 3 * V + 1) + V - 1) / V * V;
-  static constexpr int SLOT = RB * NW * PITCH;        // band rows beyond RW stay zero
+  // TMA box: the 16-byte aligned superset of a window row
+  static constexpr int BOX = (CW + V - 1 + V - 1) / V * V;
+  static constexpr int ALN = 128 / int(sizeof(T));    // 128-byte granule in elements
+  static constexpr int PITCH = (BOX + ALN - 1) / ALN * ALN;
+  // slot: front pad (reads of window col -1) + band rows; rows beyond RW stay zero.
+  // Reads reach row_off + MW + 1 <= PITCH + V + 1: a few elements into the next
+  // row (finite data with zero weights), never past the slot region's end.
+  static constexpr int SLOT = ALN + RB * NW * PITCH;
   static constexpr int P2W = KT * 32;
   static constexpr int K0N = kMaxSeg + 6;             // K0 tap rows: coarse planes ka-2 .. kb+1
   static constexpr size_t raw_bytes = size_t(NS) * SLOT * sizeof(T);
@@ -84,11 +91,11 @@ struct FLayout {
 
 template <class T, int TW1, int TW2, int NS, int MODE>
 __global__ void __launch_bounds__(512, 1)
-    k_level_fused(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ zload,
-                  T* __restrict__ gather, LevelArgs<T> a, int S0, int nt1, int nt2, int nseg,
-                  int* flag) {
+    k_level_fused(const __grid_constant__ CUtensorMap map, int64_t map_off, T* __restrict__ coef_out,
+                  T* __restrict__ zload, T* __restrict__ gather, LevelArgs<T> a, int S0, int nt1,
+                  int nt2, int nseg, int seg_base, int* flag) {
   using Lay = FLayout<T, TW1, TW2, NS>;
-  constexpr int V = Lay::V, LOGV = Lay::LOGV, PITCH = Lay::PITCH, SLOT = Lay::SLOT;
+  constexpr int V = Lay::V, PITCH = Lay::PITCH, SLOT = Lay::SLOT;
   constexpr int MW = Lay::MW, P2W = Lay::P2W, NT = Lay::NT, NW = Lay::NW, KC = Lay::KC;
   constexpr int KT = Lay::KT, RB = Lay::RB, RC = Lay::RC, SQ = Lay::SQ;
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
@@ -102,12 +109,12 @@ __global__ void __launch_bounds__(512, 1)
   T* mrow = reinterpret_cast<T*>(smem + Lay::m_off) + warp * (MW + 8);
   const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
   const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
-  const int64_t Ntot = e0 * e1 * e2, plane_sz = e1 * e2;
+  const int64_t plane_sz = e1 * e2;
   int bid = blockIdx.x;
   const int t2i = bid % nt2;
   bid /= nt2;
   const int t1i = bid % nt1;
-  const int seg = bid / nt1;
+  const int seg = seg_base + bid / nt1;
   const bool last1 = t1i == nt1 - 1, last2 = t2i == nt2 - 1, lastseg = seg == nseg - 1;
   const int64_t q1a = int64_t(t1i) * TW1, q2a = int64_t(t2i) * TW2;
   const int tw1 = last1 ? int(c1 - q1a) : TW1;
@@ -116,12 +123,8 @@ __global__ void __launch_bounds__(512, 1)
   const int64_t kb = lastseg ? c0 : ka + S0;
   const int64_t wr0 = 2 * q1a - 2, wc0 = 2 * q2a - 2;
   const int RWn = 2 * tw1 + 3, CWn = 2 * tw2 + 3;
-  const int64_t col_lo = wc0 > 0 ? wc0 : 0;
-  const int64_t col_hi = (wc0 + CWn) < e2 ? (wc0 + CWn) : e2;
-  const int ncols = int(col_hi - col_lo);
   const int64_t j0 = (2 * ka - 2) > 0 ? (2 * ka - 2) : 0;
   const int64_t jend = (2 * kb) < (e0 - 1) ? (2 * kb) : (e0 - 1);
-  const int dcol = int(col_lo - wc0);
   const int e2m = int(e2 & (V - 1));
   const bool pad0 = e0 == 1, pad1 = e1 == 1;
   // owned fine range [2qa, min(2(qa+tw), e)) in window coordinates [2, 2 + own)
@@ -172,62 +175,53 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int k = 0; k < 5; ++k) k1[q][k] = sv ? a.taps[1][(q1a + s) * 5 + k] : T(0);
   }
-  // rows this warp copies: r = warp + NW*i, element offset of col_lo within a plane
-  int64_t coff[RC];
+  // rows this warp copies: r = warp + NW*i, element offset of window col 0 in a plane
+  int64_t roff[RC];
   bool cval[RC];
+  int nvalid = 0;  // window rows inside the domain (every warp counts them all)
 #pragma unroll
   for (int i = 0; i < RC; ++i) {
     const int r = warp + NW * i;
     const int64_t g = wr0 + r;
     cval[i] = r < RWn && g >= 0 && g < e1;
-    coff[i] = g * e2 + col_lo;
+    roff[i] = g * e2 + wc0 - map_off;
   }
+  for (int r = 0; r < RWn; ++r) nvalid += (wr0 + r >= 0 && wr0 + r < e1) ? 1 : 0;
+  const uint32_t tx_bytes = uint32_t(nvalid) * Lay::BOX * uint32_t(sizeof(T));
 
-  // smem element offset of window col 0 in window row r of plane jj
-  auto plane_phase = [&](int64_t jj) {
-    return int((jj * plane_sz + wr0 * e2 + col_lo) & (V - 1));
-  };
-  auto row_off = [&](int ph, int r) { return ((ph + r * e2m) & (V - 1)) - dcol + 2 * V; };
+  // smem element offset of window col 0 in window row r of plane jj (the row's phase)
+  auto plane_phase = [&](int64_t jj) { return int((jj * plane_sz + wr0 * e2 + wc0) & (V - 1)); };
+  auto row_off = [&](int ph, int r) { return (ph + r * e2m) & (V - 1); };
 
-  // Plane window rows arrive by 16-byte cp.async (LDGSTS) from every warp. Each
-  // row copies the 16-byte aligned superset of its segment, so window col c of
-  // row r sits at smem position row_off(ph, r) + c; a chunk reaching past the
-  // array end is zero-filled (src-size < 16), nothing beyond it is read.
-  // Completion: one mbarrier per slot, every thread arrives (.noinc).
+  // Window row r of plane jj lands as the aligned box [alo, alo + BOX) at slot
+  // row r (cells before the domain start are zero-filled by the TMA; rows outside
+  // the domain are never copied and stay zero). Completion: one mbarrier per slot
+  // with one arrival (tid 0, expect_tx of the whole plane) plus the copies' bytes.
   auto issue = [&](int64_t jj) {
     const int sl = int(jj - j0) % NS;
-    T* dst = raw + sl * SLOT;
-    const int64_t pbase = jj * plane_sz;
-    const bool tail = jj == e0 - 1;  // only the last plane can reach the array end
+    T* dst = raw + sl * SLOT + Lay::ALN;
+    if (tid == 0) ptx::mbar_arrive_expect_tx(&bar[sl], tx_bytes);
+    if (lane == 0) {
+      const int64_t pbase = jj * plane_sz;
 #pragma unroll
-    for (int i = 0; i < RC; ++i) {
-      if (!cval[i]) continue;
-      const int64_t f = pbase + coff[i];
-      const int64_t alo = f & ~int64_t(V - 1);
-      const int nch = int((f - alo + ncols + V - 1) >> LOGV);
-      T* d = dst + (warp + NW * i) * PITCH + 2 * V;
-      const T* s = U + alo;
-      if (!tail) {
-        for (int ch = lane; ch < nch; ch += 32) ptx::cp_async16(d + ch * V, s + ch * V, 16);
-      } else {
-        for (int ch = lane; ch < nch; ch += 32) {
-          const int64_t rem = Ntot - (alo + int64_t(ch) * V);
-          ptx::cp_async16(d + ch * V, s + ch * V, rem >= V ? 16 : int(rem * int64_t(sizeof(T))));
-        }
+      for (int i = 0; i < RC; ++i) {
+        if (!cval[i]) continue;
+        const int64_t f = pbase + roff[i];
+        ptx::tma_load_1d(dst + (warp + NW * i) * PITCH, &map, int(f & ~int64_t(V - 1)), &bar[sl]);
       }
     }
-    ptx::cp_async_mbar_arrive(&bar[sl]);
   };
 
   // zero all buffers once: slot cells never copied (outside the domain, band
   // rows beyond the window) stay 0; K0 taps of this segment into shared memory
   for (int i = tid; i < int(Lay::k0_off / sizeof(T)); i += NT) raw[i] = T(0);
+  ptx::fence_proxy_async_smem();  // the zeros (generic proxy) before TMA writes (async proxy)
   for (int i = tid; i < Lay::K0N * 5; i += NT) {
     const int64_t ci = ka - 2 + i / 5;
     k0t[i] = (!pad0 && ci >= 0 && ci < c0 && ci <= kb + 1) ? a.taps[0][ci * 5 + i % 5] : T(0);
   }
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) ptx::mbar_init(&bar[s], NT);
+    for (int s = 0; s < NS; ++s) ptx::mbar_init(&bar[s], 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -264,7 +258,7 @@ __global__ void __launch_bounds__(512, 1)
     const int p = int(j - j0);
     const int sl = p % NS;
     ptx::mbar_wait(&bar[sl], uint32_t((p / NS) & 1));
-    const T* S = raw + sl * SLOT;
+    const T* S = raw + sl * SLOT + Lay::ALN;
     const bool jodd = j & 1;
     const int ph = plane_phase(j);
     const bool own = j >= 2 * ka && j < 2 * kb;
@@ -452,9 +446,27 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
   int S0 = kMaxSeg;
   while (S0 > 8 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
   const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
-  kern<<<unsigned(tiles * nseg), Lay::NT, Lay::total, s>>>(U, coef, z, gather, a, S0, nt1, nt2,
-                                                           nseg, flag);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  // 1D TMA coordinates are 32-bit: split the segments into launches whose planes
+  // fit below 2^31 elements from the launch's own (16-byte aligned) map base.
+  constexpr int V = Lay::V;
+  const int64_t plane_sz = a.e[1] * a.e[2], N = a.e[0] * plane_sz;
+  const int64_t lim = (int64_t(1) << 31) - 4 * int64_t(Lay::BOX);
+  int sa = 0;
+  while (sa < nseg) {
+    const int64_t p_lo = std::max<int64_t>(0, 2 * int64_t(sa) * S0 - 2);
+    int sb = sa + 1;
+    auto p_hi = [&](int sg) { return std::min<int64_t>(a.e[0] - 1, 2 * int64_t(sg) * S0 + 2 * S0); };
+    while (sb < nseg && (p_hi(sb) + 1 - p_lo) * plane_sz < lim) ++sb;
+    require((p_hi(sb - 1) + 1 - p_lo) * plane_sz < lim, "level too large for the 1D TMA path");
+    const int64_t map_off = std::max<int64_t>(0, p_lo * plane_sz - 2 * V) & ~int64_t(V - 1);
+    CUtensorMap map;
+    make_tma_1d(&map, U + map_off, uint64_t(N - map_off), int(sizeof(T)), Lay::BOX);
+    const int64_t blocks = tiles * (sb - sa);
+    kern<<<unsigned(blocks), Lay::NT, Lay::total, s>>>(map, map_off, coef, z, gather, a, S0, nt1,
+                                                       nt2, nseg, sa, flag);
+    HGR_CUDA_CHECK(cudaGetLastError());
+    sa = sb;
+  }
 }
 
 }  // namespace
@@ -462,7 +474,7 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
                         int mode, int* flag, cudaStream_t s) {
-  // cp.async needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
+  // TMA needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
   if ((reinterpret_cast<uintptr_t>(U) & 15) != 0) return false;
   if (a.e[2] < 3 || a.h[2] == nullptr) return false;
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;

@@ -60,6 +60,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 1D tensor-map copy (TMA, SASS UTMALDG) of one box starting at element x of
+// the map; completion on `bar` (complete_tx). The box start must be 16-byte
+// aligned in global memory (illegal instruction otherwise, measured on B200);
+// elements outside [0, globalDim) are zero-filled. dst 128-byte aligned.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* map, int x, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2}], [%3];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(x), "r"(smem_addr(bar))
+      : "memory");
+}
+
 // 16-byte async copy global -> shared (LDGSTS), L2 only; src_bytes < 16 zero-fills the rest.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
