@@ -1,39 +1,44 @@
 // kernels_level.cu -- fused level kernel for the fine levels: one pass over a
-// level-l array U does the GPK and the three LPK passes.
+// level-l array U does the GPK and the three LPK passes (paper kernel classes
+// 1 and 2; transforms.hpp:20-65, correction.hpp:141-154 / :238-260).
 //
-//   A CTA (16 warps) owns a (dim1, dim2) tile of coarse outputs and marches
-//   along dim 0 over a segment of coarse planes. Each fine plane's halo window
-//   arrives in shared memory through 1D TMA tensor copies (one per window row,
-//   issued by lane 0 of every warp) into an NS-slot mbarrier ring, two planes
-//   ahead. A TMA box must start 16-byte aligned, and 2^k+1 row pitches make
-//   every row's phase differ, so each row lands as its aligned superset and the
-//   consumer offsets by the row's phase. (Measured on B200 with a streaming
-//   probe, tools/mb/stream_mb.cu: warp-issued 1D TMA rows move 6.9 TB/s of
-//   unique data, 16-byte cp.async by all threads 3.4 TB/s, one issuing thread
-//   1.8 TB/s.)
-//   Each warp owns a band of 4 window rows, lanes own window columns; what a
-//   lane needs about its columns (mass stencil row, interpolation weights,
-//   ownership) is computed once per CTA and kept in registers. Slots are zeroed
-//   once and cells outside the domain carry zero weights, so the per-element
-//   work is branch- and predicate-free. One CTA barrier per plane.
-//   Per plane and row (warp-local):
-//     m = M2 u (tridiagonal mass row along dim 2 from the three neighbours each
-//       lane loads); decompose also forms the interpolant of the coarse nodes
-//       (in-plane for even planes; for odd planes the blend of the two
-//       neighbouring even planes' interpolants, which each thread keeps in
-//       registers for its own cells) and writes the coefficients U - interp of
-//       the owned nodes out of place; recompose masks the coarse nodes and
-//       gathers them into the compact level-(l-1) array;
-//     P2 = R2 m (transfer along dim 2; K2 = R2 M2 is the fused mass-trans
-//       stencil of correction.hpp:90-133).
-//   After the barrier: K1 along dim 1 (5 taps) on P2 and K0 along dim 0
-//   accumulated in registers over the rolling window of coarse planes;
-//   completed coarse planes are stored to the load vector zload.
+//   A CTA (16 warps) owns a (dim1, dim2) tile of TW1 x 64 coarse outputs and
+//   marches along dim 0 over a segment of coarse planes. Each fine plane's halo
+//   window (2*TW1+3 rows x 131 columns) arrives in shared memory through 1D TMA
+//   tensor copies, one per window row, issued by lane 0 of every warp into an
+//   NS-slot mbarrier ring. A TMA box must start 16-byte aligned and 2^k+1 row
+//   pitches give every row its own phase, so each row lands as its aligned
+//   superset and readers offset by the row's phase. (Streaming probe
+//   tools/mb/stream_mb.cu on B200: warp-issued 1D TMA rows of this geometry move
+//   7.0 TB/s of unique data; 16-byte cp.async by all threads 3.4 TB/s.)
+//
+//   Row stage (every window row of a plane): the two warp groups own coarse
+//   columns [0, 32) and [32, 64); lane L of group G owns coarse column
+//   t = 32G + L, window columns 2t..2t+4 and fine cells 2t+2, 2t+3 (loads of
+//   consecutive lanes are consecutive, so shared-memory reads are conflict
+//   free). From the five values it forms
+//     * P2 = K2 u at its coarse column (the fused mass-trans stencil K = R*M of
+//       correction.hpp:96-133 applied directly, 5 taps; in recompose mode the
+//       coarse nodes of even rows of even planes are masked, correction.hpp:251)
+//       -> shared P2 row;
+//     * decompose: the interpolant of its two cells (dim-2 blend on even rows;
+//       on odd rows the blend of the even rows above / below: the warps of a
+//       group own bands of four rows starting on an even row and look one row
+//       ahead), the coefficients u - interp of even planes and -- deferred by
+//       one plane -- of the odd plane behind it, whose interpolant blends the
+//       previous even plane's (kept in registers) with the current one
+//       (transforms.hpp:41-55 evaluated as a separable product);
+//     * recompose: the coarse nodes of even rows of even planes gathered into
+//       the compact level-(l-1) array.
+//   Column stage (the previous plane): thread (s, 2 columns) applies K1 (5
+//   taps over the P2 rows) and accumulates K0 across planes in registers; a
+//   completed coarse plane is stored to the load vector zload.
 //   Decompose applies K to U itself: K*P = M_c exactly for nested hat spaces,
 //   so M_c^-1 K U = RU + M_c^-1 K (U - P R U) = coarse + z and the three Thomas
-//   passes on zload give the corrected coarse values (refactor.hpp:48-54)
-//   directly. Recompose applies K to U with the coarse nodes masked
-//   (correction.hpp:251, the pass-0 mask).
+//   passes on zload give the corrected coarse values (refactor.hpp:48-54).
+//   The last coarse row and column of a level (and the fine row / column on
+//   them) are the faces of k_level_face, so every tile is a full TW1 x 64 block
+//   or a clipped one.
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -46,67 +51,87 @@ namespace hgrb {
 
 namespace {
 
-// Tile shapes: 4 window rows per warp; 64 (fp64) or 128 (fp32) window columns,
-// except fp32 decompose, whose per-lane interpolant registers need the
-// narrower tile to stay spill-free. fp32 recompose uses 57 coarse columns so
-// the TMA box (the row's 16-byte aligned superset) fits a 128-float pitch.
-template <class T, int MODE>
-struct FCfg {
-  static constexpr int TW1 = 29, TW2 = (sizeof(T) == 4 && MODE != kFusedDecompose) ? 57 : 29;
-  static constexpr int NS = 5;
-};
-
 constexpr int kMaxSeg = 64;  // coarse planes per dim-0 segment (S0 <= kMaxSeg)
 
-template <class T, int TW1, int TW2, int NS>
-struct FLayout {
-  static constexpr int NT = 512, NW = NT / 32;
-  static constexpr int V = 16 / int(sizeof(T));
-  static constexpr int RW = 2 * (TW1 + 1) + 3;        // max window rows
-  static constexpr int CW = 2 * (TW2 + 1) + 3;        // max window cols
-  static constexpr int KC = (CW + 31) / 32;           // column iterations per lane
-  static constexpr int KT = (TW2 + 1 + 31) / 32;      // output-column iterations
-  static constexpr int RB = 4;                        // band rows per warp
-  static_assert(RW <= RB * NW, "window rows must fit the warp bands");
-  static constexpr int RC = (RW + NW - 1) / NW;       // rows a warp copies
-  static constexpr int SQ = (TW1 + 1 + NW - 1) / NW;  // output rows per warp
-  static constexpr int MW = KC * 32;                  // row pitch of the m buffer
-  // TMA box: the 16-byte aligned superset of a window row
-  static constexpr int BOX = (CW + V - 1 + V - 1) / V * V;
-  static constexpr int ALN = 128 / int(sizeof(T));    // 128-byte granule in elements
+template <class T>
+struct LCfg {
+  static constexpr int NT = 512, NW = NT / 32, NG = 2, WG = NW / NG;
+  static constexpr int TW2 = 64;                               // coarse columns (1 per lane)
+  static constexpr int TW1 = sizeof(T) == 8 ? 14 : 16;         // coarse rows
+  static constexpr int NS = sizeof(T) == 8 ? 5 : 8;            // ring slots
+  static constexpr int V = 16 / int(sizeof(T));                // elements per 16 bytes
+  static constexpr int RW = 2 * TW1 + 3, CW = 2 * TW2 + 3;     // window rows / columns
+  static constexpr int NB = TW1 / 2;                           // bands of 4 owned rows
+  static_assert(NB <= WG, "one band per warp of a group");
+  static constexpr int BOX = (CW + V - 1 + V - 1) / V * V;     // aligned superset of a row
+  static constexpr int ALN = 128 / int(sizeof(T));             // TMA smem alignment (128 B)
   static constexpr int PITCH = (BOX + ALN - 1) / ALN * ALN;
-  // slot: front pad (reads of window col -1) + band rows; rows beyond RW stay zero.
-  // Reads reach row_off + MW + 1 <= PITCH + V + 1: a few elements into the next
-  // row (finite data with zero weights), never past the slot region's end.
-  static constexpr int SLOT = ALN + RB * NW * PITCH;
-  static constexpr int P2W = KT * 32;
-  static constexpr int K0N = kMaxSeg + 6;             // K0 tap rows: coarse planes ka-2 .. kb+1
+  static_assert(PITCH >= CW + V, "reads stay inside the row");
+  static constexpr int SLOT = RW * PITCH;
+  static constexpr int P2W = TW2;
+  static constexpr int NQ = TW1 * (TW2 / 2);                   // column-stage work items
+  static_assert(NQ <= NT, "one column-stage item per thread");
+  static constexpr int K0N = kMaxSeg + 6;                      // K0 tap rows ka-2 .. kb+1
+  static constexpr int W0N = kMaxSeg + 4;                      // dim-0 weights ka-1 .. kb+2
   static constexpr size_t raw_bytes = size_t(NS) * SLOT * sizeof(T);
-  static constexpr size_t m_off = raw_bytes;                              // per-warp m row
-  static constexpr size_t p2_off = m_off + size_t(NW) * (MW + 8) * sizeof(T);
-  static constexpr size_t k0_off = p2_off + size_t(2) * RB * NW * P2W * sizeof(T);
-  static constexpr size_t bar_off = (k0_off + size_t(K0N) * 5 * sizeof(T) + 15) / 16 * 16;
+  static constexpr size_t p2_off = raw_bytes;
+  static constexpr size_t k0_off = p2_off + size_t(2) * RW * P2W * sizeof(T);
+  static constexpr size_t w0_off = k0_off + size_t(K0N) * 5 * sizeof(T);
+  static constexpr size_t bar_off = (w0_off + size_t(2) * W0N * sizeof(T) + 15) / 16 * 16;
   static constexpr size_t total = bar_off + NS * sizeof(uint64_t);
+  static_assert(total <= 227 * 1024, "shared memory budget");
 };
 
-template <class T, int TW1, int TW2, int NS, int MODE>
-__global__ void __launch_bounds__(512, 1)
+template <class T>
+struct Vec2;
+template <>
+struct Vec2<double> { using type = double2; };
+template <>
+struct Vec2<float> { using type = float2; };
+
+// v[k] = row[pos + k], k < 5, pos = ph + (even base): pairs by 2-element vector loads
+template <class T>
+__device__ __forceinline__ void load5(const T* row, int pos, T (&v)[5]) {
+  using T2 = typename Vec2<T>::type;
+  if (!(pos & 1)) {
+    const T2 x = *reinterpret_cast<const T2*>(row + pos);
+    const T2 y = *reinterpret_cast<const T2*>(row + pos + 2);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; v[4] = row[pos + 4];
+  } else {
+    const T2 x = *reinterpret_cast<const T2*>(row + pos + 1);
+    const T2 y = *reinterpret_cast<const T2*>(row + pos + 3);
+    v[0] = row[pos]; v[1] = x.x; v[2] = x.y; v[3] = y.x; v[4] = y.y;
+  }
+}
+template <class T>
+__device__ __forceinline__ void load2(const T* row, int pos, T (&v)[2]) {
+  using T2 = typename Vec2<T>::type;
+  if (!(pos & 1)) {
+    const T2 x = *reinterpret_cast<const T2*>(row + pos);
+    v[0] = x.x; v[1] = x.y;
+  } else {
+    v[0] = row[pos]; v[1] = row[pos + 1];
+  }
+}
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(LCfg<T>::NT, 1)
     k_level_fused(const __grid_constant__ CUtensorMap map, int64_t map_off, T* __restrict__ coef_out,
                   T* __restrict__ zload, T* __restrict__ gather, LevelArgs<T> a, int S0, int nt1,
                   int nt2, int nseg, int seg_base, int* flag) {
-  using Lay = FLayout<T, TW1, TW2, NS>;
-  constexpr int V = Lay::V, PITCH = Lay::PITCH, SLOT = Lay::SLOT;
-  constexpr int MW = Lay::MW, P2W = Lay::P2W, NT = Lay::NT, NW = Lay::NW, KC = Lay::KC;
-  constexpr int KT = Lay::KT, RB = Lay::RB, RC = Lay::RC, SQ = Lay::SQ;
+  using C = LCfg<T>;
+  using T2 = typename Vec2<T>::type;
+  constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NT = C::NT;
+  constexpr int TW1 = C::TW1, TW2 = C::TW2, P2W = C::P2W, NW = C::NW, NB = C::NB, WG = C::WG;
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
   extern __shared__ __align__(128) unsigned char smem[];
   T* raw = reinterpret_cast<T*>(smem);
-  T* p2 = reinterpret_cast<T*>(smem + Lay::p2_off);
-  T* k0t = reinterpret_cast<T*>(smem + Lay::k0_off);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::bar_off);
+  T* p2 = reinterpret_cast<T*>(smem + C::p2_off);
+  T* k0t = reinterpret_cast<T*>(smem + C::k0_off);
+  T* w0t = reinterpret_cast<T*>(smem + C::w0_off);  // [2][W0N]: wl, wr of dim-0 intervals
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::bar_off);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T* mrow = reinterpret_cast<T*>(smem + Lay::m_off) + warp * (MW + 8);
   const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
   const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
   const int64_t plane_sz = e1 * e2;
@@ -115,242 +140,140 @@ __global__ void __launch_bounds__(512, 1)
   bid /= nt2;
   const int t1i = bid % nt1;
   const int seg = seg_base + bid / nt1;
-  const bool last1 = t1i == nt1 - 1, last2 = t2i == nt2 - 1, lastseg = seg == nseg - 1;
+  const bool lastseg = seg == nseg - 1;
+  // tiles cover coarse rows / columns [0, c-1); the last coarse row and column
+  // (and the fine row / column on them) are the faces of k_level_face
   const int64_t q1a = int64_t(t1i) * TW1, q2a = int64_t(t2i) * TW2;
-  const int tw1 = last1 ? int(c1 - q1a) : TW1;
-  const int tw2 = last2 ? int(c2 - q2a) : TW2;
+  const int tw1 = int(c1 - 1 - q1a < TW1 ? c1 - 1 - q1a : TW1);
+  const int tw2 = int(c2 - 1 - q2a < TW2 ? c2 - 1 - q2a : TW2);
   const int64_t ka = int64_t(seg) * S0;
   const int64_t kb = lastseg ? c0 : ka + S0;
   const int64_t wr0 = 2 * q1a - 2, wc0 = 2 * q2a - 2;
-  const int RWn = 2 * tw1 + 3, CWn = 2 * tw2 + 3;
+  const int RWn = 2 * tw1 + 3;
   const int64_t j0 = (2 * ka - 2) > 0 ? (2 * ka - 2) : 0;
   const int64_t jend = (2 * kb) < (e0 - 1) ? (2 * kb) : (e0 - 1);
-  const int e2m = int(e2 & (V - 1));
-  const bool pad0 = e0 == 1, pad1 = e1 == 1;
-  // owned fine range [2qa, min(2(qa+tw), e)) in window coordinates [2, 2 + own)
-  const int orows = 2 * tw1 - (last1 ? 1 : 0);
-  const int ocols = 2 * tw2 - (last2 ? 1 : 0);
-  const int rs = RB * warp;  // this warp's band of window rows [rs, rs + RB)
-  const bool co = lane & 1;  // parity of every column this lane owns
+  const int orows = 2 * tw1;  // owned fine rows: window rows [2, 2 + orows)
 
-  // ---- per-lane column constants (zero weights outside the domain) ----------------
-  T cml[KC], cmm[KC], cmr[KC];  // mass row (masked variant for recompose coarse rows)
-  T xml[KC], xmm[KC], xmr[KC];
-  T hl[KC], hr[KC];             // interpolation weights of odd columns
-  bool cown[KC];
+  // ---- per-lane column: coarse column t (tile-local), window columns 2t..2t+4 --------
+  const int grp = warp / WG, wg = warp % WG;
+  const int t = 32 * grp + lane;
+  const int64_t tg = q2a + t;  // global coarse column
+  const bool tvalid = t < tw2;
+  T k2[5];
 #pragma unroll
-  for (int k = 0; k < KC; ++k) {
-    const int c = lane + 32 * k;
-    const int64_t g = wc0 + c;
-    const bool in = c < CWn && g >= 0 && g < e2;
-    cown[k] = c >= 2 && c < 2 + ocols;
-    cml[k] = (in && g >= 1) ? a.h[2][g - 1] : T(0);
-    cmr[k] = (in && g + 1 < e2) ? a.h[2][g] : T(0);
-    cmm[k] = in ? T(2) * (cml[k] + cmr[k]) : T(0);
-    xml[k] = co ? T(0) : cml[k];
-    xmr[k] = co ? T(0) : cmr[k];
-    xmm[k] = co ? cmm[k] : T(0);
-    hl[k] = hr[k] = T(0);
-    if (DEC && in && co) {
-      hl[k] = a.wl[2][g >> 1];
-      hr[k] = a.wr[2][g >> 1];
+  for (int k = 0; k < 5; ++k) k2[k] = tvalid ? a.taps[2][tg * 5 + k] : T(0);
+  T hl = T(0), hr = T(0);  // interpolation weights of cell 2t+3 (odd column)
+  if (DEC && tvalid) {
+    hl = a.wl[2][tg];
+    hr = a.wr[2][tg];
+  }
+
+  // ---- per-warp row band: owned rows [b, b+4), lookahead row b+4 ---------------------
+  const bool has_band = wg < NB;
+  const int b = 2 + 4 * wg;
+  bool rown[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) rown[i] = has_band && b + i - 2 < orows && tvalid;
+  T w1l[2] = {T(0), T(0)}, w1r[2] = {T(0), T(0)};  // odd rows b+1, b+3
+  if (DEC && has_band) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int64_t gr = wr0 + b + 1 + 2 * i;
+      if (gr < e1 - 1) { w1l[i] = a.wl[1][gr >> 1]; w1r[i] = a.wr[1][gr >> 1]; }
     }
   }
-  T trl[KT], trr[KT];
-#pragma unroll
-  for (int k = 0; k < KT; ++k) {
-    const int t = lane + 32 * k;
-    trl[k] = trr[k] = T(0);
-    if (t < tw2) {
-      trl[k] = a.trl[2][q2a + t];
-      trr[k] = a.trr[2][q2a + t];
-    }
-  }
-  // output rows s = warp + NW*q: K1 taps in registers
-  T k1[SQ][5];
-#pragma unroll
-  for (int q = 0; q < SQ; ++q) {
-    const int s = warp + NW * q;
-    const bool sv = s < tw1 && !pad1;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) k1[q][k] = sv ? a.taps[1][(q1a + s) * 5 + k] : T(0);
-  }
-  // rows this warp copies: r = warp + NW*i, element offset of window col 0 in a plane
-  int64_t roff[RC];
-  bool cval[RC];
-  int nvalid = 0;  // window rows inside the domain (every warp counts them all)
-#pragma unroll
-  for (int i = 0; i < RC; ++i) {
-    const int r = warp + NW * i;
-    const int64_t g = wr0 + r;
-    cval[i] = r < RWn && g >= 0 && g < e1;
-    roff[i] = g * e2 + wc0 - map_off;
-  }
-  for (int r = 0; r < RWn; ++r) nvalid += (wr0 + r >= 0 && wr0 + r < e1) ? 1 : 0;
-  const uint32_t tx_bytes = uint32_t(nvalid) * Lay::BOX * uint32_t(sizeof(T));
+  // K-only rows outside the bands: window rows 0, 1 (and the last window row is the
+  // lookahead row of the last band)
+  const int xr0 = (wg == WG - 1) ? 0 : -1;
+  const int xr1 = (NB < WG) ? ((wg == WG - 1) ? 1 : -1) : ((wg == WG - 2) ? 1 : -1);
+  const bool krow_look = wg == NB - 1;
 
-  // smem element offset of window col 0 in window row r of plane jj (the row's phase)
-  auto plane_phase = [&](int64_t jj) { return int((jj * plane_sz + wr0 * e2 + wc0) & (V - 1)); };
-  auto row_off = [&](int ph, int r) { return (ph + r * e2m) & (V - 1); };
+  // ---- column stage item: coarse row s, columns cq, cq+1 ------------------------------
+  const bool qv = tid < C::NQ;
+  const int s = tid / (TW2 / 2), cq = 2 * (tid % (TW2 / 2));
+  T k1[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) k1[k] = (qv && s < tw1) ? a.taps[1][(q1a + s) * 5 + k] : T(0);
 
-  // Window row r of plane jj lands as the aligned box [alo, alo + BOX) at slot
-  // row r (cells before the domain start are zero-filled by the TMA; rows outside
-  // the domain are never copied and stay zero). Completion: one mbarrier per slot
-  // with one arrival (tid 0, expect_tx of the whole plane) plus the copies' bytes.
+  // ---- TMA issue: window row r of plane jj lands as its aligned box at slot row r
+  int nrows_in = 0;
+  for (int r = 0; r < RWn; ++r) nrows_in += (wr0 + r >= 0 && wr0 + r < e1) ? 1 : 0;
+  const uint32_t tx_bytes = uint32_t(nrows_in) * C::BOX * uint32_t(sizeof(T));
   auto issue = [&](int64_t jj) {
     const int sl = int(jj - j0) % NS;
-    T* dst = raw + sl * SLOT + Lay::ALN;
+    T* dst = raw + sl * SLOT;
     if (tid == 0) ptx::mbar_arrive_expect_tx(&bar[sl], tx_bytes);
     if (lane == 0) {
-      const int64_t pbase = jj * plane_sz;
-#pragma unroll
-      for (int i = 0; i < RC; ++i) {
-        if (!cval[i]) continue;
-        const int64_t f = pbase + roff[i];
-        ptx::tma_load_1d(dst + (warp + NW * i) * PITCH, &map, int(f & ~int64_t(V - 1)), &bar[sl]);
+      const int64_t pbase = jj * plane_sz + wr0 * e2 + wc0 - map_off;
+      for (int r = warp; r < RWn; r += NW) {
+        const int64_t gr = wr0 + r;
+        if (gr < 0 || gr >= e1) continue;
+        const int64_t f = pbase + int64_t(r) * e2;
+        ptx::tma_load_1d(dst + r * PITCH, &map, int(f & ~int64_t(V - 1)), &bar[sl]);
       }
     }
   };
 
-  // zero all buffers once: slot cells never copied (outside the domain, band
-  // rows beyond the window) stay 0; K0 taps of this segment into shared memory
-  for (int i = tid; i < int(Lay::k0_off / sizeof(T)); i += NT) raw[i] = T(0);
-  ptx::fence_proxy_async_smem();  // the zeros (generic proxy) before TMA writes (async proxy)
-  for (int i = tid; i < Lay::K0N * 5; i += NT) {
+  // zero the ring once (rows outside the domain are never copied and stay 0)
+  for (int i = tid; i < int(C::k0_off / sizeof(T)); i += NT) raw[i] = T(0);
+  ptx::fence_proxy_async_smem();
+  for (int i = tid; i < C::K0N * 5; i += NT) {
     const int64_t ci = ka - 2 + i / 5;
-    k0t[i] = (!pad0 && ci >= 0 && ci < c0 && ci <= kb + 1) ? a.taps[0][ci * 5 + i % 5] : T(0);
+    const int k = i % 5;
+    T v = T(0);
+    if (e0 == 1) v = (ci == 0 && k == 2) ? T(1) : T(0);
+    else if (ci >= 0 && ci < c0 && ci <= kb + 1) v = a.taps[0][ci * 5 + k];
+    k0t[i] = v;
+  }
+  for (int i = tid; i < C::W0N; i += NT) {
+    const int64_t q = ka - 1 + i;  // dim-0 interval of odd plane 2q+1
+    const bool ok = DEC && e0 > 1 && q >= 0 && q < c0 - 1;
+    w0t[i] = ok ? a.wl[0][q] : T(0);
+    w0t[C::W0N + i] = ok ? a.wr[0][q] : T(0);
   }
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) ptx::mbar_init(&bar[s], 1);
+    for (int q = 0; q < NS; ++q) ptx::mbar_init(&bar[q], 1);
     ptx::fence_mbar_init();
   }
   __syncthreads();
   const int nplanes = int(jend - j0 + 1);
   for (int p = 0; p < nplanes && p < NS; ++p) issue(j0 + p);
 
-  T accA[SQ][KT], accB[SQ][KT], accC[SQ][KT];
-#pragma unroll
-  for (int q = 0; q < SQ; ++q)
-#pragma unroll
-    for (int k = 0; k < KT; ++k) accA[q][k] = accB[q][k] = accC[q][k] = T(0);
-  // interpolant of the last two even planes at this thread's (row, column)
-  // cells (decompose): odd planes blend them. A thread keeps the same cells
-  // for every plane, so they stay in registers.
-  T ipA[RB][KC], ipB[RB][KC];
-#pragma unroll
-  for (int ib = 0; ib < RB; ++ib)
-#pragma unroll
-    for (int k = 0; k < KC; ++k) ipA[ib][k] = ipB[ib][k] = T(0);
-  bool bad = false;
-  int pb = 0;
-
-  auto load3 = [&](const T* rp, T (&u)[KC], T (&ul)[KC], T (&ur)[KC]) {
-#pragma unroll
-    for (int k = 0; k < KC; ++k) {
-      const int c = lane + 32 * k;
-      u[k] = rp[c];
-      ul[k] = rp[c - 1];
-      ur[k] = rp[c + 1];
-    }
+  const int e2m = int(e2 & (V - 1));
+  const int ph00 = int((wr0 * e2 + wc0) & (V - 1));
+  // shared-memory position of window column 2t in row r of plane jj
+  auto pos = [&](int64_t jj, int r) {
+    return int((jj * plane_sz + ph00 + int64_t(r) * e2m) & (V - 1)) + 2 * t;
   };
 
-  auto process = [&](int64_t j) {
-    const int p = int(j - j0);
-    const int sl = p % NS;
-    ptx::mbar_wait(&bar[sl], uint32_t((p / NS) & 1));
-    const T* S = raw + sl * SLOT + Lay::ALN;
-    const bool jodd = j & 1;
-    const int ph = plane_phase(j);
-    const bool own = j >= 2 * ka && j < 2 * kb;
-    // even planes whose interpolant an owned odd plane needs (incl. plane 2kb)
-    const bool needip = DEC && !jodd && j >= 2 * ka && j <= 2 * kb;
-    T w0l = T(0), w0r = T(0);
-    if (DEC && jodd && own) {
-      w0l = a.wl[0][j >> 1];
-      w0r = a.wr[0][j >> 1];
-    }
-    T* P2 = p2 + pb * (RB * NW * P2W);
-    T u[KC], ul[KC], ur[KC], hprev[KC];
-    load3(S + rs * PITCH + row_off(ph, rs), u, ul, ur);
+  T acc0[2], acc1[2], acc2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc0[k] = acc1[k] = acc2[k] = T(0);
+  T A1p[4][2];  // interpolant of the previous even plane at this lane's band cells
+#pragma unroll
+  for (int i = 0; i < 4; ++i) A1p[i][0] = A1p[i][1] = T(0);
+  T bad = T(0);
 
-#pragma unroll
-    for (int ib = 0; ib < RB; ++ib) {
-      const int r = rs + ib;
-      const int64_t gr = wr0 + r;
-      const bool ro = r & 1;  // window and global row parities agree (wr0 even)
-      const bool rown = own && r >= 2 && r < 2 + orows;
-      if (REC && !jodd && !ro) {  // coarse nodes of this row read as zero
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-          mrow[lane + 32 * k] = xmm[k] * u[k] + xml[k] * ul[k] + xmr[k] * ur[k];
-        if (rown) {  // gather the coarse nodes of this row into C_{l-1}
-          const T* rp = S + r * PITCH + row_off(ph, r);
-          T* gdst = gather + ((j >> 1) * c1 + (gr >> 1)) * c2 + q2a;
-          for (int t = lane; t < tw2; t += 32) gdst[t] = rp[2 + 2 * t];
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-          mrow[lane + 32 * k] = cmm[k] * u[k] + cml[k] * ul[k] + cmr[k] * ur[k];
-      }
-      // next row's values (also the even row below an odd row, for its interpolant)
-      T nu[KC], nl[KC], nr[KC];
-      load3(S + (r + 1) * PITCH + row_off(ph, r + 1), nu, nl, nr);
-      if (DEC) {
-        T* orow = coef_out + (j * e1 + gr) * e2 + wc0;
-        const bool ripr = needip && r >= 2 && r <= 2 + orows && gr < e1;
-        if (ripr) {
-#pragma unroll
-          for (int k = 0; k < KC; ++k) {
-            T ip;
-            if (!ro) {  // even row: interp along dim 2
-              ip = co ? hl[k] * ul[k] + hr[k] * ur[k] : u[k];
-              hprev[k] = ip;
-            } else {    // odd row: from the even rows above / below
-              const T hn = co ? hl[k] * nl[k] + hr[k] * nr[k] : nu[k];
-              ip = a.wl[1][gr >> 1] * hprev[k] + a.wr[1][gr >> 1] * hn;
-            }
-            ipB[ib][k] = ip;
-            if (rown && cown[k]) {
-              orow[lane + 32 * k] = u[k] - ip;
-              bad |= !isfinite(u[k]);
-            }
-          }
-        } else if (jodd && rown) {  // odd plane: blend of the neighbouring even planes
-#pragma unroll
-          for (int k = 0; k < KC; ++k) {
-            const T ip = w0l * ipA[ib][k] + w0r * ipB[ib][k];
-            if (cown[k]) {
-              orow[lane + 32 * k] = u[k] - ip;
-              bad |= !isfinite(u[k]);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      // P2 = R2 m for this row
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        const int t = lane + 32 * k;
-        P2[r * P2W + t] = mrow[2 * t + 2] + trl[k] * mrow[2 * t + 1] + trr[k] * mrow[2 * t + 3];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        u[k] = nu[k];
-        ul[k] = nl[k];
-        ur[k] = nr[k];
-      }
-    }
-    __syncthreads();
+  auto k2dot = [&](const T (&v)[5], bool masked) {
+    if (REC && masked) return k2[1] * v[1] + k2[3] * v[3];
+    return k2[0] * v[0] + k2[1] * v[1] + k2[2] * v[2] + k2[3] * v[3] + k2[4] * v[4];
+  };
 
-    // ---- K1 along dim 1 (5 taps), K0 accumulated across planes
-    const int64_t E = jodd ? j + 1 : j;
+  // column stage for plane jj: K1 over the P2 rows, K0 into the accumulators
+  auto column_stage = [&](int64_t jj) {
+    if (!qv) return;
+    const T* P2 = p2 + (jj & 1) * (C::RW * P2W) + 2 * s * P2W + cq;
+    T P0 = T(0), P1 = T(0);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const T2 x = *reinterpret_cast<const T2*>(P2 + k * P2W);
+      P0 += k1[k] * x.x;
+      P1 += k1[k] * x.y;
+    }
+    const int64_t E = (jj & 1) ? jj + 1 : jj;
     const int ib0 = int(E / 2 - 1 - (ka - 2));  // K0 table row of coarse plane E/2 - 1
     T kA, kB, kC;
-    if (pad0) {
-      kA = T(0); kB = T(1); kC = T(0);
-    } else if (!jodd) {
+    if (!(jj & 1)) {
       kA = k0t[ib0 * 5 + 4];
       kB = k0t[(ib0 + 1) * 5 + 2];
       kC = k0t[(ib0 + 2) * 5 + 0];
@@ -359,114 +282,245 @@ __global__ void __launch_bounds__(512, 1)
       kB = k0t[(ib0 + 1) * 5 + 1];
       kC = T(0);
     }
+    acc0[0] += kA * P0; acc0[1] += kA * P1;
+    acc1[0] += kB * P0; acc1[1] += kB * P1;
+    acc2[0] += kC * P0; acc2[1] += kC * P1;
+  };
+  // store coarse plane i (acc0) if this segment owns it, then rotate
+  auto flush = [&](int64_t i) {
+    if (qv && i >= ka && i < kb && s < tw1) {
+      T* zr = zload + (i * c1 + q1a + s) * c2 + q2a + cq;
+      if (cq < tw2) zr[0] = acc0[0];
+      if (cq + 1 < tw2) zr[1] = acc0[1];
+    }
 #pragma unroll
-    for (int q = 0; q < SQ; ++q) {
-      const int s = warp + NW * q;
-      if (s < tw1) {
+    for (int k = 0; k < 2; ++k) {
+      acc0[k] = acc1[k];
+      acc1[k] = acc2[k];
+      acc2[k] = T(0);
+    }
+  };
+
+  for (int64_t j = j0; j <= jend; ++j) {
+    const int p = int(j - j0);
+    const int sl = p % NS;
+    ptx::mbar_wait(&bar[sl], uint32_t((p / NS) & 1));
+    const T* S = raw + sl * SLOT;
+    T* P2 = p2 + (j & 1) * (C::RW * P2W) + t;
+    const bool jodd = j & 1;
+
+    // ---- row stage ----
 #pragma unroll
-        for (int k = 0; k < KT; ++k) {
-          const int t = lane + 32 * k;
-          T P;
-          if (pad1) {
-            P = P2[2 * P2W + t];
-          } else {
-            const T* pc = P2 + (2 * s) * P2W + t;
-            P = k1[q][0] * pc[0] + k1[q][1] * pc[P2W] + k1[q][2] * pc[2 * P2W] +
-                k1[q][3] * pc[3 * P2W] + k1[q][4] * pc[4 * P2W];
+    for (int xi = 0; xi < 2; ++xi) {  // K-only rows 0, 1
+      const int xr = xi ? xr1 : xr0;
+      if (xr >= 0) {
+        T v[5];
+        load5<T>(S + xr * PITCH, pos(j, xr), v);
+        P2[xr * P2W] = k2dot(v, !jodd && !(xr & 1));
+      }
+    }
+    if (has_band) {
+      if (jodd || !DEC) {
+        // K path only (odd planes; recompose / load-only modes)
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const int r = b + i;
+          if (i == 4 && !krow_look) break;
+          T v[5];
+          load5<T>(S + r * PITCH, pos(j, r), v);
+          const bool masked = !jodd && !(r & 1);
+          P2[r * P2W] = k2dot(v, masked);
+          if (REC && masked && i < 4 && rown[i] && j >= 2 * ka && j < 2 * kb)
+            gather[((j >> 1) * c1 + ((wr0 + r) >> 1)) * c2 + tg] = v[2];  // coarse node -> C_{l-1}
+        }
+      } else {
+        // decompose, even plane j: K path, coefficients of j and of the odd
+        // plane j-1 behind it (deferred), interpolants kept for plane j+1
+        const bool own_e = j >= 2 * ka && j < 2 * kb;
+        const bool own_o = j > j0 && j - 1 >= 2 * ka && j - 1 < 2 * kb;
+        const int iw = int(((j - 1) >> 1) - (ka - 1));
+        const T w0l = own_o ? w0t[iw] : T(0), w0r = own_o ? w0t[C::W0N + iw] : T(0);
+        const T* So = raw + ((p + NS - 1) % NS) * SLOT;  // slot of plane j-1
+        T* orow_e = coef_out + (j * e1 + wr0 + b) * e2 + wc0 + 2 * t + 2;
+        T* orow_o = orow_e - plane_sz;
+        T A2e[3][2];  // dim-2 interpolants of the even rows b, b+2, b+4
+        // row order b, b+2, b+1, b+4, b+3: odd rows see both even neighbours
+#pragma unroll
+        for (int step = 0; step < 5; ++step) {
+          const int i = step == 0 ? 0 : step == 1 ? 2 : step == 2 ? 1 : step == 3 ? 4 : 3;
+          const int r = b + i;
+          T v[5];
+          load5<T>(S + r * PITCH, pos(j, r), v);
+          if (i < 4 || krow_look) P2[r * P2W] = k2dot(v, false);
+          if (!(i & 1)) {
+            A2e[i >> 1][0] = v[2];
+            A2e[i >> 1][1] = hl * v[2] + hr * v[4];
           }
-          accA[q][k] += kA * P;
-          accB[q][k] += kB * P;
-          accC[q][k] += kC * P;
+          if (i == 4) continue;
+          T A1[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            A1[k] = (i & 1) ? w1l[i >> 1] * A2e[i >> 1][k] + w1r[i >> 1] * A2e[(i >> 1) + 1][k]
+                            : A2e[i >> 1][k];
+          if (rown[i]) {
+            if (own_e) {
+              const T c0v = v[2] - A1[0], c1v = v[3] - A1[1];
+              bad = c0v * T(0) + bad;
+              bad = c1v * T(0) + bad;
+              T* o = orow_e + int64_t(i) * e2;
+              o[0] = c0v;
+              o[1] = c1v;
+            }
+            if (own_o) {
+              T u[2];
+              load2<T>(So + r * PITCH, pos(j - 1, r) + 2, u);
+              const T c0v = u[0] - (w0l * A1p[i][0] + w0r * A1[0]);
+              const T c1v = u[1] - (w0l * A1p[i][1] + w0r * A1[1]);
+              bad = c0v * T(0) + bad;
+              bad = c1v * T(0) + bad;
+              T* o = orow_o + int64_t(i) * e2;
+              o[0] = c0v;
+              o[1] = c1v;
+            }
+          }
+          A1p[i][0] = A1[0];
+          A1p[i][1] = A1[1];
         }
       }
     }
-    pb ^= 1;
-  };
-
-  auto flush = [&](int64_t i) {
-    if (i < ka || i >= kb) return;
-#pragma unroll
-    for (int q = 0; q < SQ; ++q) {
-      const int s = warp + NW * q;
-      if (s >= tw1) continue;
-      T* zr = zload + (i * c1 + q1a + s) * c2 + q2a;
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        const int t = lane + 32 * k;
-        if (t < tw2) zr[t] = accA[q][k];
-      }
+    // ---- column stage of the previous plane ----
+    if (j > j0) {
+      column_stage(j - 1);
+      if (!((j - 1) & 1)) flush((j - 1) / 2 - 1);
     }
-  };
+    __syncthreads();
+    // the slot of plane j-1 is free now (its last reader ran in this phase)
+    if (j > j0 && j - 1 + NS <= jend) issue(j - 1 + NS);
+  }
+  column_stage(jend);
+  flush(jend / 2 - 1);
+  flush(jend / 2);
+  if (DEC && flag) {
+    const bool nf = !(bad == T(0));
+    if (__syncthreads_or(nf) && tid == 0) atomicOr(flag, 1);
+  }
+}
 
-  for (int64_t E = j0; E <= jend; E += 2) {
-    process(E);
-    if (E > j0) process(E - 1);
-    flush(E / 2 - 1);
-    if (DEC) {
-#pragma unroll
-      for (int ib = 0; ib < RB; ++ib)
-#pragma unroll
-        for (int k = 0; k < KC; ++k) ipA[ib][k] = ipB[ib][k];
-    }
-#pragma unroll
-    for (int q = 0; q < SQ; ++q)
-#pragma unroll
-      for (int k = 0; k < KT; ++k) {
-        accA[q][k] = accB[q][k];
-        accB[q][k] = accC[q][k];
-        accC[q][k] = T(0);
+// Faces outside the tiles of k_level_fused: zload on the last coarse column
+// (c2-1, every coarse (i0, i1)) and the last coarse row (c1-1, i2 < c2-1) --
+// K0 (x) K1 (x) K2 applied directly, coarse nodes masked in recompose mode
+// (correction.hpp:251) -- plus, in decompose mode, the coefficients of the fine
+// cells on the last fine column / row (transforms.hpp:20-65), and in recompose
+// mode the gather of the coarse nodes on those faces. One thread per item.
+template <class T, int MODE>
+__global__ void __launch_bounds__(256)
+    k_level_face(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ zload,
+                 T* __restrict__ gather, LevelArgs<T> a, int* flag) {
+  constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
+  const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
+  const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
+  const int64_t nA = c0 * c1, nB = c0 * (c2 - 1);
+  const int64_t fA = DEC ? e0 * e1 : 0, fB = DEC ? e0 * (e2 - 1) : 0;
+  const int64_t total = nA + nB + fA + fB;
+  auto coarse = [&](int64_t b0, int64_t b1, int64_t b2) {
+    return U[((2 * b0) * e1 + 2 * b1) * e2 + 2 * b2];
+  };
+  for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < total;
+       it += int64_t(gridDim.x) * blockDim.x) {
+    if (it < nA + nB) {
+      int64_t i0, i1, i2;
+      if (it < nA) {
+        i0 = it / c1; i1 = it % c1; i2 = c2 - 1;
+      } else {
+        const int64_t q = it - nA;
+        i0 = q / (c2 - 1); i1 = c1 - 1; i2 = q % (c2 - 1);
       }
-    if (E > j0) {  // slots of planes E-2, E-1 are free (barrier inside process(E-1))
-      if (E - 2 + NS <= jend) issue(E - 2 + NS);
-      if (E - 1 + NS <= jend) issue(E - 1 + NS);
+      T acc = T(0);
+      for (int x = 0; x < 5; ++x) {
+        const int64_t f0 = 2 * i0 - 2 + x;
+        if (f0 < 0 || f0 >= e0) continue;
+        const T w0 = e0 == 1 ? T(1) : a.taps[0][i0 * 5 + x];
+        T acc1 = T(0);
+        for (int y = 0; y < 5; ++y) {
+          const int64_t f1 = 2 * i1 - 2 + y;
+          if (f1 < 0 || f1 >= e1) continue;
+          const T* row = U + (f0 * e1 + f1) * e2;
+          T acc2 = T(0);
+          for (int z = 0; z < 5; ++z) {
+            const int64_t f2 = 2 * i2 - 2 + z;
+            if (f2 < 0 || f2 >= e2) continue;
+            const bool masked = REC && !((f0 | f1 | f2) & 1);
+            acc2 += a.taps[2][i2 * 5 + z] * (masked ? T(0) : row[f2]);
+          }
+          acc1 += a.taps[1][i1 * 5 + y] * acc2;
+        }
+        acc += w0 * acc1;
+      }
+      const int64_t q = (i0 * c1 + i1) * c2 + i2;
+      zload[q] = acc;
+      if (REC) gather[q] = coarse(i0, i1, i2);
+    } else if (DEC) {
+      int64_t q = it - nA - nB, j, r, c;
+      if (q < fA) {
+        j = q / e1; r = q % e1; c = e2 - 1;
+      } else {
+        q -= fA;
+        j = q / (e2 - 1); r = e1 - 1; c = q % (e2 - 1);
+      }
+      const int64_t idx = (j * e1 + r) * e2 + c;
+      const T u = U[idx];
+      if (flag && !isfinite(u)) atomicOr(flag, 1);
+      if ((j | r | c) & 1) coef_out[idx] = u - interp_node(a, j, r, c, coarse);
     }
   }
-  flush(jend / 2);
-  if (DEC && flag && __syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
 }
 
 template <class T, int MODE>
 void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int* flag,
                cudaStream_t s) {
-  using Cfg = FCfg<T, MODE>;
-  constexpr int TW1 = Cfg::TW1, TW2 = Cfg::TW2, NS = Cfg::NS;
-  using Lay = FLayout<T, TW1, TW2, NS>;
-  auto kern = k_level_fused<T, TW1, TW2, NS, MODE>;
+  using C = LCfg<T>;
+  auto kern = k_level_fused<T, MODE>;
   static int attr_dev = -1;
   int dev = 0;
   HGR_CUDA_CHECK(cudaGetDevice(&dev));
   if (attr_dev != dev) {
     HGR_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(Lay::total)));
+                                        int(C::total)));
     attr_dev = dev;
   }
-  const int nt1 = int(std::max<int64_t>(1, (a.c[1] - 1 + TW1 - 1) / TW1));
-  const int nt2 = int(std::max<int64_t>(1, (a.c[2] - 1 + TW2 - 1) / TW2));
+  const int nt1 = int((a.c[1] - 1 + C::TW1 - 1) / C::TW1);
+  const int nt2 = int((a.c[2] - 1 + C::TW2 - 1) / C::TW2);
   const int64_t tiles = int64_t(nt1) * nt2;
   int S0 = kMaxSeg;
   while (S0 > 8 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
   const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
   // 1D TMA coordinates are 32-bit: split the segments into launches whose planes
   // fit below 2^31 elements from the launch's own (16-byte aligned) map base.
-  constexpr int V = Lay::V;
+  constexpr int V = C::V;
   const int64_t plane_sz = a.e[1] * a.e[2], N = a.e[0] * plane_sz;
-  const int64_t lim = (int64_t(1) << 31) - 4 * int64_t(Lay::BOX);
+  const int64_t lim = (int64_t(1) << 31) - 4 * int64_t(C::BOX);
   int sa = 0;
   while (sa < nseg) {
     const int64_t p_lo = std::max<int64_t>(0, 2 * int64_t(sa) * S0 - 2);
+    auto p_hi = [&](int sg) {
+      return std::min<int64_t>(a.e[0] - 1, 2 * int64_t(sg) * S0 + 2 * S0);
+    };
     int sb = sa + 1;
-    auto p_hi = [&](int sg) { return std::min<int64_t>(a.e[0] - 1, 2 * int64_t(sg) * S0 + 2 * S0); };
     while (sb < nseg && (p_hi(sb) + 1 - p_lo) * plane_sz < lim) ++sb;
     require((p_hi(sb - 1) + 1 - p_lo) * plane_sz < lim, "level too large for the 1D TMA path");
     const int64_t map_off = std::max<int64_t>(0, p_lo * plane_sz - 2 * V) & ~int64_t(V - 1);
     CUtensorMap map;
-    make_tma_1d(&map, U + map_off, uint64_t(N - map_off), int(sizeof(T)), Lay::BOX);
+    make_tma_1d(&map, U + map_off, uint64_t(N - map_off), int(sizeof(T)), C::BOX);
     const int64_t blocks = tiles * (sb - sa);
-    kern<<<unsigned(blocks), Lay::NT, Lay::total, s>>>(map, map_off, coef, z, gather, a, S0, nt1,
-                                                       nt2, nseg, sa, flag);
+    kern<<<unsigned(blocks), C::NT, C::total, s>>>(map, map_off, coef, z, gather, a, S0, nt1, nt2,
+                                                   nseg, sa, flag);
     HGR_CUDA_CHECK(cudaGetLastError());
     sa = sb;
   }
+  const int64_t face_items = a.c[0] * (a.c[1] + a.c[2] - 1) +
+                             (MODE == kFusedDecompose ? a.e[0] * (a.e[1] + a.e[2] - 1) : 0);
+  k_level_face<T, MODE><<<grid_for(face_items, 256), 256, 0, s>>>(U, coef, z, gather, a, flag);
+  HGR_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace
@@ -476,7 +530,7 @@ bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const Leve
                         int mode, int* flag, cudaStream_t s) {
   // TMA needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
   if ((reinterpret_cast<uintptr_t>(U) & 15) != 0) return false;
-  if (a.e[2] < 3 || a.h[2] == nullptr) return false;
+  if (a.e[1] < 3 || a.e[2] < 3 || a.h[2] == nullptr) return false;  // 1D: reference path
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
   if (mode == kFusedDecompose)
     run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, a, flag, s);

@@ -15,7 +15,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
 
 using T = double;
-constexpr int NT = 512;
+#define NT ((int)blockDim.x)
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(c) : "memory"); }
@@ -36,7 +36,7 @@ __device__ __forceinline__ void cpa_arrive(uint64_t* b) { asm volatile("cp.async
 struct Geo { int64_t e; int RW, CW, step_r, step_c, S; int nt1, nt2, nseg; int P; int B; };
 
 template <int MODE, int NS>
-__global__ void __launch_bounds__(NT, 1) k_stream(const T* U, const __grid_constant__ CUtensorMap map, Geo g, T* sink) {
+__global__ void __launch_bounds__(512, 1) k_stream(const T* U, const __grid_constant__ CUtensorMap map, Geo g, T* sink) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int SLOT = g.RW * g.P;
   T* raw = reinterpret_cast<T*>(smem);
@@ -112,16 +112,14 @@ int main(int argc, char** argv) {
   auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   struct Case { int mode; int RW, CW, step_r, step_c; const char* name; };
-  std::vector<Case> cases = {
-      {0, 61, 62, 58, 58, "TMA1d 1 issuer, 61x62"},
-      {3, 61, 62, 58, 58, "TMA1d warp issuers, 61x62"},
-      {1, 61, 62, 58, 58, "cp.async16, 61x62"},
-      {2, 61, 62, 58, 58, "LDG direct, 61x62"},
-      {0, 19, 256, 16, 252, "TMA1d 1 issuer, 19x256"},
-      {3, 19, 256, 16, 252, "TMA1d warp issuers, 19x256"},
-      {3, 35, 128, 32, 124, "TMA1d warp issuers, 35x128"},
-      {1, 35, 128, 32, 124, "cp.async16, 35x128"},
-  };
+  std::vector<Case> cases;
+  int nthr = 512;
+  if (argc >= 7) {
+    cases.push_back({atoi(argv[1]), atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), atoi(argv[5]), "custom"});
+    nthr = atoi(argv[6]);
+  } else {
+    cases = {{3, 61, 62, 58, 58, "TMA1d warp issuers, 61x62"}, {1, 61, 62, 58, 58, "cp.async16, 61x62"}};
+  }
   for (auto& cs : cases) {
     CUtensorMap map;
     cuuint64_t gdim[1] = {cuuint64_t(N)}, gstr[1] = {0};
@@ -136,15 +134,15 @@ int main(int argc, char** argv) {
       g.nt2 = int((e - 3 + cs.step_c - 1) / cs.step_c);
       g.nseg = int((e + S - 1) / S);
       const int grid = g.nt1 * g.nt2 * g.nseg;
-      constexpr int NS = 4;
+      constexpr int NS = 5;
       size_t smem = size_t(NS) * cs.RW * g.P * sizeof(T) + 64;
       if (smem > 227 * 1024) { printf("%s: smem too big\n", cs.name); continue; }
       auto run = [&]() {
         switch (cs.mode) {
-          case 0: CK(cudaFuncSetAttribute(k_stream<0, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); k_stream<0, NS><<<grid, NT, smem>>>(U, map, g, sink); break;
-          case 1: CK(cudaFuncSetAttribute(k_stream<1, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); k_stream<1, NS><<<grid, NT, smem>>>(U, map, g, sink); break;
-          case 2: k_stream<2, NS><<<grid, NT, 0>>>(U, map, g, sink); break;
-          case 3: CK(cudaFuncSetAttribute(k_stream<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); k_stream<3, NS><<<grid, NT, smem>>>(U, map, g, sink); break;
+          case 0: CK(cudaFuncSetAttribute(k_stream<0, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); k_stream<0, NS><<<grid, nthr, smem>>>(U, map, g, sink); break;
+          case 1: CK(cudaFuncSetAttribute(k_stream<1, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); k_stream<1, NS><<<grid, nthr, smem>>>(U, map, g, sink); break;
+          case 2: k_stream<2, NS><<<grid, nthr, 0>>>(U, map, g, sink); break;
+          case 3: CK(cudaFuncSetAttribute(k_stream<3, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))); k_stream<3, NS><<<grid, nthr, smem>>>(U, map, g, sink); break;
         }
       };
       run(); CK(cudaDeviceSynchronize());
