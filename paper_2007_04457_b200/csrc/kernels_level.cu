@@ -199,18 +199,30 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
   int nrows_in = 0;
   for (int r = 0; r < RWn; ++r) nrows_in += (wr0 + r >= 0 && wr0 + r < e1) ? 1 : 0;
   const uint32_t tx_bytes = uint32_t(nrows_in) * C::BOX * uint32_t(sizeof(T));
+  // per issuing lane (lane 0 of warp w: rows w, w+NW, ...): 32-bit TMA coordinate of
+  // window column 0 of the row in plane 0 (relative to the map base)
+  constexpr int RPW = (C::RW + NW - 1) / NW;
+  // (arithmetic modulo 2^32: the true coordinates of a launch lie in [-2, 2^31))
+  uint32_t rc[RPW];
+  unsigned rvalid = 0;
+#pragma unroll
+  for (int i = 0; i < RPW; ++i) {
+    const int r = warp + NW * i;
+    const int64_t gr = wr0 + r;
+    rc[i] = uint32_t(uint64_t(gr * e2 + wc0 - map_off));
+    if (r < RWn && gr >= 0 && gr < e1) rvalid |= 1u << i;
+  }
   auto issue = [&](int64_t jj) {
     const int sl = int(jj - j0) % NS;
-    T* dst = raw + sl * SLOT;
     if (tid == 0) ptx::mbar_arrive_expect_tx(&bar[sl], tx_bytes);
     if (lane == 0) {
-      const int64_t pbase = jj * plane_sz + wr0 * e2 + wc0 - map_off;
-      for (int r = warp; r < RWn; r += NW) {
-        const int64_t gr = wr0 + r;
-        if (gr < 0 || gr >= e1) continue;
-        const int64_t f = pbase + int64_t(r) * e2;
-        ptx::tma_load_1d(dst + r * PITCH, &map, int(f & ~int64_t(V - 1)), &bar[sl]);
-      }
+      T* dst = raw + sl * SLOT + warp * PITCH;
+      const uint32_t pb = uint32_t(uint64_t(jj * plane_sz));
+#pragma unroll
+      for (int i = 0; i < RPW; ++i)
+        if (rvalid & (1u << i))
+          ptx::tma_load_1d(dst + i * NW * PITCH, &map, int((pb + rc[i]) & ~uint32_t(V - 1)),
+                           &bar[sl]);
     }
   };
 
@@ -241,10 +253,9 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
 
   const int e2m = int(e2 & (V - 1));
   const int ph00 = int((wr0 * e2 + wc0) & (V - 1));
-  // shared-memory position of window column 2t in row r of plane jj
-  auto pos = [&](int64_t jj, int r) {
-    return int((jj * plane_sz + ph00 + int64_t(r) * e2m) & (V - 1)) + 2 * t;
-  };
+  // shared-memory position of window column 2t in row r of a plane with phase phj
+  auto plane_ph = [&](int64_t jj) { return int((jj * plane_sz + ph00) & (V - 1)); };
+  auto pos = [&](int phj, int r) { return ((phj + r * e2m) & (V - 1)) + 2 * t; };
 
   T acc0[2], acc1[2], acc2[2];
 #pragma unroll
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
 
   auto k2dot = [&](const T (&v)[5], bool masked) {
     if (REC && masked) return k2[1] * v[1] + k2[3] * v[3];
-    return k2[0] * v[0] + k2[1] * v[1] + k2[2] * v[2] + k2[3] * v[3] + k2[4] * v[4];
+    return (k2[0] * v[0] + k2[1] * v[1] + k2[2] * v[2]) + (k2[3] * v[3] + k2[4] * v[4]);
   };
 
   // column stage for plane jj: K1 over the P2 rows, K0 into the accumulators
@@ -308,6 +319,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
     const T* S = raw + sl * SLOT;
     T* P2 = p2 + (j & 1) * (C::RW * P2W) + t;
     const bool jodd = j & 1;
+    const int phj = plane_ph(j), phm = plane_ph(j - 1);
 
     // ---- row stage ----
 #pragma unroll
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
       const int xr = xi ? xr1 : xr0;
       if (xr >= 0) {
         T v[5];
-        load5<T>(S + xr * PITCH, pos(j, xr), v);
+        load5<T>(S + xr * PITCH, pos(phj, xr), v);
         P2[xr * P2W] = k2dot(v, !jodd && !(xr & 1));
       }
     }
@@ -327,7 +339,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
           const int r = b + i;
           if (i == 4 && !krow_look) break;
           T v[5];
-          load5<T>(S + r * PITCH, pos(j, r), v);
+          load5<T>(S + r * PITCH, pos(phj, r), v);
           const bool masked = !jodd && !(r & 1);
           P2[r * P2W] = k2dot(v, masked);
           if (REC && masked && i < 4 && rown[i] && j >= 2 * ka && j < 2 * kb)
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
           const int i = step == 0 ? 0 : step == 1 ? 2 : step == 2 ? 1 : step == 3 ? 4 : 3;
           const int r = b + i;
           T v[5];
-          load5<T>(S + r * PITCH, pos(j, r), v);
+          load5<T>(S + r * PITCH, pos(phj, r), v);
           if (i < 4 || krow_look) P2[r * P2W] = k2dot(v, false);
           if (!(i & 1)) {
             A2e[i >> 1][0] = v[2];
@@ -373,7 +385,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
             }
             if (own_o) {
               T u[2];
-              load2<T>(So + r * PITCH, pos(j - 1, r) + 2, u);
+              load2<T>(So + r * PITCH, pos(phm, r) + 2, u);
               const T c0v = u[0] - (w0l * A1p[i][0] + w0r * A1[0]);
               const T c1v = u[1] - (w0l * A1p[i][1] + w0r * A1[1]);
               bad = c0v * T(0) + bad;
