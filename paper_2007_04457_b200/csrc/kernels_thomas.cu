@@ -1,22 +1,27 @@
 // kernels_thomas.cu -- IPK: batched Thomas solves of the mass matrix
 // (ThomasSolver::solve_fiber, correction.hpp:202-208; thomas_pass :262-278).
 //
-// Forward elimination f_i = x_i - m_{i-1} f_{i-1} and back substitution
-// y_i = (f_i - u_i y_{i+1}) / p_i are first-order affine recurrences. A line is
-// cut into chunks held in registers; each chunk computes its local result with
-// a zero carry plus the product of its recurrence coefficients, the chunk
-// carries are combined by an exact affine scan, and every chunk then re-runs
-// the reference recurrence from its true carry. One HBM read and one write per
-// element per dimension; no second pass over the forward-eliminated values.
-// The factor tables (identical for every line of a (level, dim)) live in
-// shared memory.
+// Forward elimination y_i = x_i - m_{i-1} y_{i-1} and back substitution
+// z_i = (y_i - u_i z_{i+1}) / p_i are first-order affine recurrences whose
+// coefficients are the same for every line of a (level, dimension). A line is
+// cut into NC chunks held in registers, one chunk per thread:
+//   g = local forward result with zero carry;  y = g + P * c_f
+//   h = local backward result of y with zero carry;  z = h + Q * c_b
+// where P_i = prod_{k=s..i} (-m_{k-1}) and Q_i = prod_{k=i..e-1} (-u_k / p_k)
+// are line-independent tables built once per CTA, and the chunk carries c_f
+// (= y at the position before the chunk) and c_b (= z after it) come from an
+// exact affine scan over the chunk summaries in shared memory. One HBM read
+// and one write per element per dimension, five flops per element.
 //
-//   dims 0/1 (strided lines): persistent CTAs; a group = 32 consecutive lines
-//     along the contiguous dim (lanes) x the whole line (warps own chunks).
-//     The next group is prefetched by cp.async into shared memory while the
-//     current one is solved; carries combine through shared memory.
-//   dim 2 (contiguous rows): one warp per row, lanes own chunks; rows are
-//     double-buffered in shared memory by cp.async; carries by warp shuffles.
+//   k_thomas_lines (dims 0 / 1, strided lines): a group = 32 consecutive
+//     lines along the contiguous dimension (lanes) x the whole line (16 warps,
+//     one chunk each). Every thread streams its own chunk of the next group
+//     into a private shared-memory landing zone with cp.async while it solves
+//     the current group from registers; stores are coalesced rows.
+//   k_thomas_rows (dim 2, contiguous rows): a group = R consecutive rows, a
+//     contiguous block moved by one bulk copy (TMA engine) into a double-buffered
+//     shared-memory tile; each row is cut into 16*32/R chunks spread over the
+//     lanes; results go back through the tile and one bulk store.
 #include "kernels_fused.cuh"
 #include "plan.hpp"
 #include "ptx.cuh"
@@ -25,132 +30,99 @@ namespace hgrb {
 
 namespace {
 
+// Line-independent tables for NC chunks of CH positions over a line of n:
+//   tm[i] = m_{i-1} (0 at i = 0 and i >= n), tp[i] = 1/p_i, tu[i] = u_i (0 at
+//   i >= n-1), P (forward carry products), Q (backward carry products);
+//   positions >= n have tp = 0 so padding never feeds back.
 template <class T>
-__device__ __forceinline__ T shfl_up(T v, int d) {
-  return __shfl_up_sync(0xffffffffu, v, d);
-}
-template <class T>
-__device__ __forceinline__ T shfl_down(T v, int d) {
-  return __shfl_down_sync(0xffffffffu, v, d);
-}
-
-// tables: tm[i] = mult[i] (i < n-1), tr[i] = 1/pivot[i], tu[i] = upper[i] (i < n-1)
-template <class T>
-__device__ __forceinline__ void load_tables(T* tm, T* tr, T* tu, const T* mult, const T* rpiv,
-                                            const T* upper, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    tr[i] = rpiv[i];
-    tm[i] = i + 1 < n ? mult[i] : T(0);
-    tu[i] = i + 1 < n ? upper[i] : T(0);
+__device__ void build_tables(T* tm, T* tP, T* tp, T* tu, T* tQ, int n, int NC, int CH,
+                             const T* mult, const T* rpiv, const T* upper) {
+  const int NP = NC * CH;
+  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
+    tm[i] = (i >= 1 && i < n) ? mult[i - 1] : T(0);
+    tp[i] = i < n ? rpiv[i] : T(0);
+    tu[i] = i < n - 1 ? upper[i] : T(0);
   }
-}
-
-// forward pass of chunk [s0, s0+cnt): local result (zero carry) + carry coefficient
-template <class T, int CH>
-__device__ __forceinline__ void fwd_local(const T (&x)[CH], int s0, int cnt, const T* tm, T& g,
-                                          T& A) {
-  g = T(0);
-  A = T(1);
-#pragma unroll
-  for (int k = 0; k < CH; ++k) {
-    if (k < cnt) {
-      const int i = s0 + k;
-      if (i == 0) {
-        g = x[k];
-      } else {
-        const T m = tm[i - 1];
-        g = x[k] - m * g;
-        A *= -m;
-      }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NC; q += blockDim.x) {
+    const int s = q * CH;
+    T a = T(1);
+    for (int k = 0; k < CH; ++k) {
+      a *= -tm[s + k];
+      tP[s + k] = a;
+    }
+    T b = T(1);
+    for (int k = CH - 1; k >= 0; --k) {
+      b *= -(tu[s + k] * tp[s + k]);
+      tQ[s + k] = b;
     }
   }
+  __syncthreads();
 }
 
 template <class T, int CH>
-__device__ __forceinline__ void fwd_apply(T (&x)[CH], int s0, int cnt, const T* tm, T carry) {
-  T prev = carry;
+struct ChunkSolve {
+  // forward local (zero carry) in place; returns the chunk's last value
+  static __device__ __forceinline__ T fwd_local(T (&x)[CH], const T* tm) {
+    T g = T(0);
 #pragma unroll
-  for (int k = 0; k < CH; ++k) {
-    if (k < cnt) {
-      const int i = s0 + k;
-      if (i > 0) x[k] = x[k] - tm[i - 1] * prev;
-      prev = x[k];
+    for (int k = 0; k < CH; ++k) {
+      g = x[k] - tm[k] * g;
+      x[k] = g;
     }
+    return g;
   }
-}
-
-template <class T, int CH>
-__device__ __forceinline__ void bwd_local(const T (&x)[CH], int s0, int cnt, int n, const T* tr,
-                                          const T* tu, T& h, T& B) {
-  h = T(0);
-  B = T(1);
+  static __device__ __forceinline__ void apply(T (&x)[CH], const T* tab, T c) {
 #pragma unroll
-  for (int k = CH - 1; k >= 0; --k) {
-    if (k < cnt) {
-      const int i = s0 + k;
-      const T rp = tr[i];
-      if (i == n - 1) {
-        h = x[k] * rp;
-      } else {
-        const T u = tu[i];
-        h = (x[k] - u * h) * rp;
-        B *= -u * rp;
-      }
-    }
+    for (int k = 0; k < CH; ++k) x[k] += tab[k] * c;
   }
-}
-
-template <class T, int CH>
-__device__ __forceinline__ void bwd_apply(T (&x)[CH], int s0, int cnt, int n, const T* tr,
-                                          const T* tu, T carry) {
-  T next = carry;
+  // backward local (zero carry) in place; returns the chunk's first value
+  static __device__ __forceinline__ T bwd_local(T (&x)[CH], const T* tu, const T* tp) {
+    T h = T(0);
 #pragma unroll
-  for (int k = CH - 1; k >= 0; --k) {
-    if (k < cnt) {
-      const int i = s0 + k;
-      x[k] = (i == n - 1) ? x[k] * tr[i] : (x[k] - tu[i] * next) * tr[i];
-      next = x[k];
+    for (int k = CH - 1; k >= 0; --k) {
+      h = (x[k] - tu[k] * h) * tp[k];
+      x[k] = h;
     }
+    return h;
   }
-}
+};
 
 // ---- strided lines (dims 0 / 1) ---------------------------------------------------
 
-template <class T, int CH, int W>
-__global__ void __launch_bounds__(32 * W, 1)
-    k_thomas_strided(const T* in, T* out, int64_t e0, int64_t e1, int64_t e2, int dim,
-                     const T* __restrict__ mult, const T* __restrict__ rpiv,
-                     const T* __restrict__ upper, int64_t ngroups) {
-  constexpr int NT = 32 * W, NMAX = W * CH;
-  extern __shared__ __align__(16) unsigned char smem_t[];
-  T* buf = reinterpret_cast<T*>(smem_t);          // [NMAX][32]
-  T* tm = buf + NMAX * 32;
-  T* tr = tm + NMAX;
-  T* tu = tr + NMAX;
-  T* sg = tu + NMAX;                               // [W][32]
-  T* sa = sg + W * 32;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int n = int(dim == 0 ? e0 : e1);
-  const int64_t sd = dim == 0 ? e1 * e2 : e2;
-  const int64_t so = dim == 0 ? e2 : e1 * e2;  // stride of the other strided dim
-  const int64_t nblk2 = (e2 + 31) / 32;
-  load_tables(tm, tr, tu, mult, rpiv, upper, n);
-  const int s0 = w * CH;
-  int cnt = n - s0;
-  cnt = cnt < 0 ? 0 : (cnt > CH ? CH : cnt);
+constexpr int kLW = 16;  // warps (= chunks per line) of k_thomas_lines
 
-  auto group_base = [&](int64_t g, int& nl) {
-    const int64_t ia = g / nblk2, i2 = (g % nblk2) * 32;
-    nl = int(e2 - i2 < 32 ? e2 - i2 : 32);
-    return ia * so + i2;
+template <class T, int CH>
+__global__ void __launch_bounds__(32 * kLW, 1)
+    k_thomas_lines(const T* in, T* out, int n, int64_t sd, int64_t so, int64_t c2, int nblk2,
+                   int64_t ngroups, const T* __restrict__ mult, const T* __restrict__ rpiv,
+                   const T* __restrict__ upper) {
+  constexpr int NT = 32 * kLW, NC = kLW, NP = NC * CH;
+  extern __shared__ __align__(16) unsigned char smem_t[];
+  T* tm = reinterpret_cast<T*>(smem_t);
+  T* tP = tm + NP;
+  T* tp = tP + NP;
+  T* tu = tp + NP;
+  T* tQ = tu + NP;
+  T* sf = tQ + NP;         // [NC][32] forward chunk summaries
+  T* sb = sf + NC * 32;    // [NC][32] backward chunk summaries
+  T* land = sb + NC * 32;  // [CH][NT] per-thread landing zone
+  build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int s0 = w * CH;
+
+  auto line_off = [&](int64_t g, bool& valid) {
+    const int64_t ia = g / nblk2, ib = g - ia * nblk2;
+    valid = ib * 32 + lane < c2;
+    return ia * so + ib * 32 + lane;
   };
   auto prefetch = [&](int64_t g) {
-    int nl;
-    const int64_t base = group_base(g, nl);
-    for (int idx = tid; idx < n * 32; idx += NT) {
-      const int i = idx >> 5, q = idx & 31;
-      const bool ok = q < nl;
-      ptx::cp_async_elem<int(sizeof(T))>(buf + idx, in + base + i * sd + (ok ? q : 0),
+    bool valid;
+    const T* src = in + line_off(g, valid) + int64_t(s0) * sd;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const bool ok = valid && s0 + k < n;
+      ptx::cp_async_elem<int(sizeof(T))>(land + k * NT + tid, ok ? src + k * sd : in,
                                          ok ? int(sizeof(T)) : 0);
     }
     ptx::cp_async_commit();
@@ -160,115 +132,133 @@ __global__ void __launch_bounds__(32 * W, 1)
   if (g < ngroups) prefetch(g);
   for (; g < ngroups; g += gridDim.x) {
     ptx::cp_async_wait_all();
-    __syncthreads();
     T x[CH];
 #pragma unroll
-    for (int k = 0; k < CH; ++k)
-      if (k < cnt) x[k] = buf[(s0 + k) * 32 + lane];
-    __syncthreads();
+    for (int k = 0; k < CH; ++k) x[k] = land[k * NT + tid];
     if (g + gridDim.x < ngroups) prefetch(g + gridDim.x);
 
-    T gl, A;
-    fwd_local<T, CH>(x, s0, cnt, tm, gl, A);
-    sg[w * 32 + lane] = gl;
-    sa[w * 32 + lane] = A;
+    // forward: local solve, exact carry scan over the chunks before this one
+    sf[w * 32 + lane] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
     __syncthreads();
-    T carry = T(0);
-    for (int v = 0; v < w; ++v) carry = sg[v * 32 + lane] + sa[v * 32 + lane] * carry;
-    fwd_apply<T, CH>(x, s0, cnt, tm, carry);
-    T h, B;
-    bwd_local<T, CH>(x, s0, cnt, n, tr, tu, h, B);
+    T c = T(0);
+    for (int v = 0; v < w; ++v) c = sf[v * 32 + lane] + tP[v * CH + CH - 1] * c;
+    ChunkSolve<T, CH>::apply(x, tP + s0, c);
+    // backward: local solve, carry scan over the chunks after this one
+    sb[w * 32 + lane] = ChunkSolve<T, CH>::bwd_local(x, tu + s0, tp + s0);
     __syncthreads();
-    sg[w * 32 + lane] = h;
-    sa[w * 32 + lane] = B;
-    __syncthreads();
-    carry = T(0);
-    for (int v = W - 1; v > w; --v) carry = sg[v * 32 + lane] + sa[v * 32 + lane] * carry;
-    bwd_apply<T, CH>(x, s0, cnt, n, tr, tu, carry);
-    int nl;
-    const int64_t base = group_base(g, nl);
-    if (lane < nl) {
+    c = T(0);
+    for (int v = NC - 1; v > w; --v) c = sb[v * 32 + lane] + tQ[v * CH] * c;
+    ChunkSolve<T, CH>::apply(x, tQ + s0, c);
+
+    bool valid;
+    T* dst = out + line_off(g, valid) + int64_t(s0) * sd;
+    if (valid) {
 #pragma unroll
       for (int k = 0; k < CH; ++k)
-        if (k < cnt) out[base + (s0 + k) * sd + lane] = x[k];
+        if (s0 + k < n) dst[k * sd] = x[k];
     }
   }
 }
 
 // ---- contiguous rows (dim 2) --------------------------------------------------------
 
-template <class T, int CH>
-__global__ void __launch_bounds__(256) k_thomas_rows(const T* in, T* out, int64_t rows, int n,
-                                                     const T* __restrict__ mult,
-                                                     const T* __restrict__ rpiv,
-                                                     const T* __restrict__ upper) {
-  constexpr int PITCH = 32 * CH + 1, NMAX = 32 * CH;
+template <class T, int CH, int R>
+struct RowsCfg {
+  static constexpr int NT = 512, NW = NT / 32;
+  static constexpr int CPW = 32 / R;         // chunks per warp
+  static constexpr int NC = NW * CPW;        // chunks per row
+  static constexpr int NP = NC * CH;
+  // the tile holds R rows of n; the last row's padded chunk positions read up to NP past its start
+  static __host__ __device__ size_t buf_elems(int n) {
+    return (size_t(R - 1) * n + (NP > n ? NP : n) + 15) / 16 * 16;
+  }
+  static size_t smem(int n) {
+    return (size_t(5) * NP + size_t(2) * NC * R + 2 * buf_elems(n)) * sizeof(T) + 16 + 2 * 8;
+  }
+};
+
+template <class T, int CH, int R>
+__global__ void __launch_bounds__(512, 1)
+    k_thomas_rows(const T* in, T* out, int64_t rows, int n, const T* __restrict__ mult,
+                  const T* __restrict__ rpiv, const T* __restrict__ upper) {
+  using C = RowsCfg<T, CH, R>;
+  constexpr int NC = C::NC, NP = C::NP, CPW = C::CPW;
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
-  T* tr = tm + NMAX;
-  T* tu = tr + NMAX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  T* bufs = tu + NMAX + warp * 2 * PITCH;
-  load_tables(tm, tr, tu, mult, rpiv, upper, n);
+  T* tP = tm + NP;
+  T* tp = tP + NP;
+  T* tu = tp + NP;
+  T* tQ = tu + NP;
+  T* sf = tQ + NP;       // [NC][R]
+  T* sb = sf + NC * R;   // [NC][R]
+  const size_t BE = C::buf_elems(n);
+  T* buf0 = reinterpret_cast<T*>(
+      (reinterpret_cast<uintptr_t>(sb + NC * R) + 15) & ~uintptr_t(15));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(buf0 + 2 * BE);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int r = lane % R, q = w * CPW + lane / R, s0 = q * CH;
+  const int64_t ngroups = (rows + R - 1) / R;
+
+  // zero both tiles once: positions past a row's end then read finite data
+  for (size_t i = tid; i < 2 * BE; i += blockDim.x) buf0[i] = T(0);
+  build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
+  if (tid == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::fence_proxy_async_smem();
   __syncthreads();
-  const int s0 = lane * CH;
-  int cnt = n - s0;
-  cnt = cnt < 0 ? 0 : (cnt > CH ? CH : cnt);
-  const int64_t stride = int64_t(gridDim.x) * 8;
-  auto prefetch = [&](int64_t row, T* dst) {
-    const T* src = in + row * n;
-    for (int i = lane; i < n; i += 32)
-      ptx::cp_async_elem<int(sizeof(T))>(dst + i, src + i, int(sizeof(T)));
+
+  auto gbytes = [&](int64_t g) {
+    const int64_t nr = (rows - g * R) < R ? (rows - g * R) : R;
+    return uint32_t((uint64_t(nr) * n * sizeof(T) + 15) & ~uint64_t(15));
   };
-  int64_t row = int64_t(blockIdx.x) * 8 + warp;
-  if (row < rows) prefetch(row, bufs);
-  ptx::cp_async_commit();
-  for (int it = 0; row < rows; row += stride, ++it) {
-    T* cur = bufs + (it & 1) * PITCH;
-    T* nxt = bufs + ((it + 1) & 1) * PITCH;
-    if (row + stride < rows) prefetch(row + stride, nxt);
-    ptx::cp_async_commit();
-    ptx::cp_async_wait_group<1>();
-    __syncwarp();
+  auto load = [&](int64_t g, int b) {  // tid 0 only
+    const uint32_t by = gbytes(g);
+    ptx::mbar_arrive_expect_tx(&bar[b], by);
+    ptx::bulk_g2s(buf0 + b * BE, in + g * R * int64_t(n), by, &bar[b]);
+  };
+  int64_t g = blockIdx.x;
+  if (tid == 0) {
+    if (g < ngroups) load(g, 0);
+    if (g + gridDim.x < ngroups) load(g + gridDim.x, 1);
+  }
+  for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
+    const int b = it & 1;
+    T* tile = buf0 + b * BE;
+    ptx::mbar_wait(&bar[b], uint32_t((it >> 1) & 1));
+    T* mine = tile + r * n + s0;
     T x[CH];
 #pragma unroll
-    for (int k = 0; k < CH; ++k)
-      if (k < cnt) x[k] = cur[s0 + k];
-    T g, A;
-    fwd_local<T, CH>(x, s0, cnt, tm, g, A);
-    // inclusive affine scan over lanes: F_t = G_t + A_t F_{t-1}
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const T gp = shfl_up(g, d), ap = shfl_up(A, d);
-      if (lane >= d) {
-        g = g + A * gp;
-        A = A * ap;
-      }
-    }
-    T carry = shfl_up(g, 1);
-    if (lane == 0) carry = T(0);
-    fwd_apply<T, CH>(x, s0, cnt, tm, carry);
-    T h, B;
-    bwd_local<T, CH>(x, s0, cnt, n, tr, tu, h, B);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const T hn = shfl_down(h, d), bn = shfl_down(B, d);
-      if (lane + d < 32) {
-        h = h + B * hn;
-        B = B * bn;
-      }
-    }
-    T next = shfl_down(h, 1);
-    if (lane == 31) next = T(0);
-    bwd_apply<T, CH>(x, s0, cnt, n, tr, tu, next);
+    for (int k = 0; k < CH; ++k) x[k] = mine[k];
+
+    sf[q * R + r] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
+    __syncthreads();
+    T c = T(0);
+    for (int v = 0; v < q; ++v) c = sf[v * R + r] + tP[v * CH + CH - 1] * c;
+    ChunkSolve<T, CH>::apply(x, tP + s0, c);
+    sb[q * R + r] = ChunkSolve<T, CH>::bwd_local(x, tu + s0, tp + s0);
+    __syncthreads();
+    c = T(0);
+    for (int v = NC - 1; v > q; --v) c = sb[v * R + r] + tQ[v * CH] * c;
+    ChunkSolve<T, CH>::apply(x, tQ + s0, c);
+
 #pragma unroll
     for (int k = 0; k < CH; ++k)
-      if (k < cnt) cur[s0 + k] = x[k];
-    __syncwarp();
-    T* dst = out + row * n;
-    for (int i = lane; i < n; i += 32) dst[i] = cur[i];
-    __syncwarp();
+      if (s0 + k < n) mine[k] = x[k];
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      ptx::bulk_s2g(out + g * R * int64_t(n), tile, gbytes(g));
+      ptx::bulk_commit();
+      if (g + 2 * int64_t(gridDim.x) < ngroups) {
+        ptx::bulk_wait_read0();  // the store has read the tile; refill it
+        load(g + 2 * int64_t(gridDim.x), b);
+      }
+    }
   }
+  if (tid == 0) ptx::bulk_wait0();
 }
 
 int sm_count() {
@@ -282,42 +272,47 @@ int sm_count() {
   return sms;
 }
 
-template <class T, int CH>
-void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const T* rpiv,
-              const T* upper, cudaStream_t s) {
-  const size_t smem = size_t(3 * 32 * CH + 8 * 2 * (32 * CH + 1)) * sizeof(T);
-  static int attr_dev = -1;
+// raise a kernel's dynamic shared-memory limit once per (device, kernel, size)
+void set_smem_attr(const void* fn, size_t bytes) {
+  struct Seen { int dev; const void* fn; size_t bytes; };
+  static thread_local Seen seen[64];
+  static thread_local int nseen = 0;
   int dev = 0;
   HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    HGR_CUDA_CHECK(cudaFuncSetAttribute(k_thomas_rows<T, CH>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_dev = dev;
-  }
-  const int64_t want = (rows + 7) / 8;
-  const int grid = int(want < int64_t(sm_count()) * 3 ? want : int64_t(sm_count()) * 3);
-  k_thomas_rows<T, CH><<<grid, 256, smem, s>>>(in, out, rows, int(n), mult, rpiv, upper);
+  for (int i = 0; i < nseen; ++i)
+    if (seen[i].dev == dev && seen[i].fn == fn && seen[i].bytes >= bytes) return;
+  HGR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  if (nseen < 64) seen[nseen++] = Seen{dev, fn, bytes};
+}
+
+template <class T, int CH, int R>
+void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const T* rpiv,
+              const T* upper, cudaStream_t s) {
+  using C = RowsCfg<T, CH, R>;
+  const size_t smem = C::smem(int(n));
+  auto kern = k_thomas_rows<T, CH, R>;
+  set_smem_attr(reinterpret_cast<const void*>(kern), smem);
+  const int64_t groups = (rows + R - 1) / R;
+  const int grid = int(groups < sm_count() ? groups : sm_count());
+  kern<<<grid, C::NT, smem, s>>>(in, out, rows, int(n), mult, rpiv, upper);
   HGR_CUDA_CHECK(cudaGetLastError());
 }
 
 template <class T, int CH>
-void run_strided(const T* in, T* out, const int64_t e[3], int dim, const T* mult,
-                 const T* rpiv, const T* upper, cudaStream_t s) {
-  constexpr int W = 16;
-  const size_t smem = size_t(W * CH * 32 + 3 * W * CH + 2 * W * 32) * sizeof(T);
-  static int attr_dev = -1;
-  int dev = 0;
-  HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    HGR_CUDA_CHECK(cudaFuncSetAttribute(k_thomas_strided<T, CH, W>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_dev = dev;
-  }
+void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, const T* rpiv,
+               const T* upper, cudaStream_t s) {
+  constexpr int NT = 32 * kLW, NP = kLW * CH;
+  const size_t smem = (size_t(5) * NP + 2 * kLW * 32 + size_t(CH) * NT) * sizeof(T);
+  auto kern = k_thomas_lines<T, CH>;
+  set_smem_attr(reinterpret_cast<const void*>(kern), smem);
+  const int n = int(e[dim]);
+  const int64_t sd = dim == 0 ? e[1] * e[2] : e[2];
+  const int64_t so = dim == 0 ? e[2] : e[1] * e[2];  // stride of the other strided dim
   const int64_t na = dim == 0 ? e[1] : e[0];
-  const int64_t groups = na * ((e[2] + 31) / 32);
+  const int nblk2 = int((e[2] + 31) / 32);
+  const int64_t groups = na * nblk2;
   const int grid = int(groups < sm_count() ? groups : sm_count());
-  k_thomas_strided<T, CH, W><<<grid, 32 * W, smem, s>>>(in, out, e[0], e[1], e[2], dim, mult,
-                                                         rpiv, upper, groups);
+  kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, e[2], nblk2, groups, mult, rpiv, upper);
   HGR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -327,21 +322,26 @@ template <class T>
 bool launch_thomas_fast(const T* in, T* out, const int64_t e[3], int dim, const T* mult,
                         const T* rpiv, const T* upper, cudaStream_t s) {
   const int64_t n = e[dim];
+  if (n < 2) return false;
   if (dim == 2) {
+    // bulk copies need 16-byte aligned group blocks
+    if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+      return false;
     const int64_t rows = e[0] * e[1];
-    if (n <= 32 * 2) run_rows<T, 2>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 5) run_rows<T, 5>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 9) run_rows<T, 9>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 17) run_rows<T, 17>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 33) run_rows<T, 33>(in, out, rows, n, mult, rpiv, upper, s);
+    if (n <= 32 * 2) run_rows<T, 2, 16>(in, out, rows, n, mult, rpiv, upper, s);
+    else if (n <= 32 * 5) run_rows<T, 5, 16>(in, out, rows, n, mult, rpiv, upper, s);
+    else if (n <= 32 * 9) run_rows<T, 9, 16>(in, out, rows, n, mult, rpiv, upper, s);
+    else if (n <= 32 * 17) run_rows<T, 17, 16>(in, out, rows, n, mult, rpiv, upper, s);
+    else if (sizeof(T) == 4 && n <= 32 * 33) run_rows<T, 33, 16>(in, out, rows, n, mult, rpiv, upper, s);
+    else if (n <= 64 * 17) run_rows<T, 17, 8>(in, out, rows, n, mult, rpiv, upper, s);
     else return false;
     return true;
   }
-  if (n <= 16 * 2) run_strided<T, 2>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= 16 * 5) run_strided<T, 5>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= 16 * 9) run_strided<T, 9>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= 16 * 17) run_strided<T, 17>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= 16 * 33) run_strided<T, 33>(in, out, e, dim, mult, rpiv, upper, s);
+  if (n <= kLW * 2) run_lines<T, 2>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 5) run_lines<T, 5>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 9) run_lines<T, 9>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 17) run_lines<T, 17>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 33) run_lines<T, 33>(in, out, e, dim, mult, rpiv, upper, s);
   else return false;
   return true;
 }
