@@ -92,10 +92,14 @@ struct ChunkSolve {
 
 constexpr int kLW = 16;  // warps (= chunks per line) of k_thomas_lines
 
+// Groups: "full" groups (ia, ib) cover lines ib*32 .. ib*32+31 along dim 2 of
+// row ia of the other strided dim; when c2 % 32 != 0 the remaining columns
+// form "tail" groups whose lanes take 32 consecutive ia at one column. All
+// offsets are 32-bit (the launcher requires < 2^31 elements).
 template <class T, int CH>
 __global__ void __launch_bounds__(32 * kLW, 1)
-    k_thomas_lines(const T* in, T* out, int n, int64_t sd, int64_t so, int64_t c2, int nblk2,
-                   int64_t ngroups, const T* __restrict__ mult, const T* __restrict__ rpiv,
+    k_thomas_lines(const T* in, T* out, int n, int sd, int so, int na, int c2, int nfull,
+                   int ntail, int ngroups, const T* __restrict__ mult, const T* __restrict__ rpiv,
                    const T* __restrict__ upper) {
   constexpr int NT = 32 * kLW, NC = kLW, NP = NC * CH;
   extern __shared__ __align__(16) unsigned char smem_t[];
@@ -110,32 +114,39 @@ __global__ void __launch_bounds__(32 * kLW, 1)
   build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s0 = w * CH;
+  const int kmax = n - s0 < CH ? n - s0 : CH;  // valid positions of this warp's chunk
+  const int nfull_groups = na * nfull;
 
-  auto line_off = [&](int64_t g, bool& valid) {
-    const int64_t ia = g / nblk2, ib = g - ia * nblk2;
-    valid = ib * 32 + lane < c2;
-    return ia * so + ib * 32 + lane;
+  // element offset of position s0 of this lane's line in group g (-1: no line)
+  auto line_off = [&](int g) {
+    if (g < nfull_groups) {
+      const int ia = int(unsigned(g) / unsigned(nfull)), ib = g - ia * nfull;
+      return ia * so + ib * 32 + lane + s0 * sd;
+    }
+    const int t = g - nfull_groups;  // tail: 32 rows ia at column c2 - ntail + (t % ntail)
+    const int ia = (t / ntail) * 32 + lane, col = c2 - ntail + t % ntail;
+    return ia < na ? ia * so + col + s0 * sd : -1;
   };
-  auto prefetch = [&](int64_t g) {
-    bool valid;
-    const T* src = in + line_off(g, valid) + int64_t(s0) * sd;
+  auto prefetch = [&](int g) {
+    const int off = line_off(g);
+    const T* src = in + (off < 0 ? 0 : off);
 #pragma unroll
     for (int k = 0; k < CH; ++k) {
-      const bool ok = valid && s0 + k < n;
-      ptx::cp_async_elem<int(sizeof(T))>(land + k * NT + tid, ok ? src + k * sd : in,
-                                         ok ? int(sizeof(T)) : 0);
+      const bool ok = off >= 0 && k < kmax;
+      ptx::cp_async_elem<int(sizeof(T))>(land + k * NT + tid, src, ok ? int(sizeof(T)) : 0);
+      if (k + 1 < kmax) src += sd;
     }
     ptx::cp_async_commit();
   };
 
-  int64_t g = blockIdx.x;
+  int g = blockIdx.x;
   if (g < ngroups) prefetch(g);
   for (; g < ngroups; g += gridDim.x) {
     ptx::cp_async_wait_all();
     T x[CH];
 #pragma unroll
     for (int k = 0; k < CH; ++k) x[k] = land[k * NT + tid];
-    if (g + gridDim.x < ngroups) prefetch(g + gridDim.x);
+    if (g + int(gridDim.x) < ngroups) prefetch(g + gridDim.x);
 
     // forward: local solve, exact carry scan over the chunks before this one
     sf[w * 32 + lane] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
@@ -150,12 +161,14 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     for (int v = NC - 1; v > w; --v) c = sb[v * 32 + lane] + tQ[v * CH] * c;
     ChunkSolve<T, CH>::apply(x, tQ + s0, c);
 
-    bool valid;
-    T* dst = out + line_off(g, valid) + int64_t(s0) * sd;
-    if (valid) {
+    const int off = line_off(g);
+    if (off >= 0) {
+      T* dst = out + off;
 #pragma unroll
-      for (int k = 0; k < CH; ++k)
-        if (s0 + k < n) dst[k * sd] = x[k];
+      for (int k = 0; k < CH; ++k) {
+        if (k < kmax) *dst = x[k];
+        dst += sd;
+      }
     }
   }
 }
@@ -306,13 +319,14 @@ void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, 
   auto kern = k_thomas_lines<T, CH>;
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int n = int(e[dim]);
-  const int64_t sd = dim == 0 ? e[1] * e[2] : e[2];
-  const int64_t so = dim == 0 ? e[2] : e[1] * e[2];  // stride of the other strided dim
-  const int64_t na = dim == 0 ? e[1] : e[0];
-  const int nblk2 = int((e[2] + 31) / 32);
-  const int64_t groups = na * nblk2;
-  const int grid = int(groups < sm_count() ? groups : sm_count());
-  kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, e[2], nblk2, groups, mult, rpiv, upper);
+  const int sd = int(dim == 0 ? e[1] * e[2] : e[2]);
+  const int so = int(dim == 0 ? e[2] : e[1] * e[2]);  // stride of the other strided dim
+  const int na = int(dim == 0 ? e[1] : e[0]);
+  const int c2 = int(e[2]);
+  const int nfull = c2 / 32, ntail = c2 % 32;
+  const int groups = na * nfull + ((na + 31) / 32) * ntail;
+  const int grid = groups < sm_count() ? groups : sm_count();
+  kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, na, c2, nfull, ntail, groups, mult, rpiv, upper);
   HGR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -337,6 +351,7 @@ bool launch_thomas_fast(const T* in, T* out, const int64_t e[3], int dim, const 
     else return false;
     return true;
   }
+  if (e[0] * e[1] * e[2] >= (int64_t(1) << 31)) return false;  // 32-bit offsets
   if (n <= kLW * 2) run_lines<T, 2>(in, out, e, dim, mult, rpiv, upper, s);
   else if (n <= kLW * 5) run_lines<T, 5>(in, out, e, dim, mult, rpiv, upper, s);
   else if (n <= kLW * 9) run_lines<T, 9>(in, out, e, dim, mult, rpiv, upper, s);
