@@ -1,97 +1,364 @@
-// kernels_interp.cu -- recompose interpolation (GPK^-1, refactor.hpp:77-87).
+// kernels_interp.cu -- recompose interpolation (GPK^-1, refactor.hpp:77-87):
+// out[coarse] = C - Z, out[refined] = coef + interp(C - Z), or the
+// interpolation alone for classes above the recompose prefix.
 //
-// k_interp_rec: one thread per fine column, streaming down the fine rows of a
-// (planes x rows) tile; the corrected coarse block (C - Z) sits in shared
-// memory, the in-plane interpolant of odd rows is formed from the two even
-// rows held in registers. out[coarse] = C - Z, out[refined] = coef + interp
-// (or interp alone for classes above the recompose prefix). In-place safe.
+// k_interp_march: a CTA (16 warps) owns a (dim1, dim2) tile of TW1 x 64 coarse
+// cells (2*TW1 x 128 fine cells) and marches along dim 0 over a segment of
+// coarse planes. Per coarse plane m the corrected coarse window (C and Z rows
+// by 1D TMA copies) gives, for every thread's cells, the in-plane interpolant
+// of fine plane 2m (dim-2 blend on even rows, blend of the even rows above /
+// below on odd rows), kept in registers; the odd fine plane 2m-1 blends it
+// with plane m-1's (transforms.hpp:41-55 evaluated as a separable product).
+// Coefficient planes stream through an NS-slot TMA ring (rows land as their
+// 16-byte aligned supersets, read at the row's phase); outputs are coalesced
+// row stores. Lane L of column group G owns coarse column t = 32G + L and fine
+// cells 2t, 2t+1; the warps of a group own bands of four fine rows. In-place
+// safe (every cell is read before it is written, by the CTA that owns it).
+// The last fine row and column of the level are the faces of k_interp_face.
 #include <algorithm>
 
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
 #include "plan.hpp"
+#include "ptx.cuh"
+#include "tma.hpp"
 
 namespace hgrb {
 
 namespace {
 
-// ---- recompose interpolation -------------------------------------------------
+constexpr int kMaxSegI = 32;  // coarse planes per dim-0 segment
 
-template <class T, int B0, int B1, int B2>
-__global__ void __launch_bounds__(2 * B2) k_interp_rec(const T* coef, T* out, const T* __restrict__ C,
-                                                       const T* __restrict__ Z, LevelArgs<T> a,
-                                                       bool with, int nb1, int nb2) {
-  constexpr int NT = 2 * B2, S1 = B1 + 1, S2 = B2 + 2;
-  extern __shared__ __align__(16) unsigned char smem_i[];
-  T* cs = reinterpret_cast<T*>(smem_i);  // (B0+1) x S1 x S2 corrected coarse block
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int bid = blockIdx.x;
-  const int b2 = bid % nb2;
-  bid /= nb2;
-  const int b1 = bid % nb1;
-  const int b0 = bid / nb1;
-  const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
-  const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
-  const int64_t qa0 = int64_t(b0) * B0, qa1 = int64_t(b1) * B1, qa2 = int64_t(b2) * B2;
-  const int nb0 = int((c0 - 1 + B0 - 1) / B0) > 0 ? int((c0 - 1 + B0 - 1) / B0) : 1;
-  const int tb0 = b0 == nb0 - 1 ? int(c0 - qa0) : B0;
-  const int tb1 = b1 == nb1 - 1 ? int(c1 - qa1) : B1;
-  const int tb2 = b2 == nb2 - 1 ? int(c2 - qa2) : B2;
-  const int n0 = int(std::min<int64_t>(tb0 + 1, c0 - qa0));
-  const int n1 = int(std::min<int64_t>(tb1 + 1, c1 - qa1));
-  const int n2 = int(std::min<int64_t>(tb2 + 1, c2 - qa2));
-  // corrected coarse block C - Z: rows (x0, x1) over warps, columns over lanes
-  for (int row = warp; row < n0 * n1; row += NT / 32) {
-    const int x0 = row / n1, x1 = row - x0 * n1;
-    const int64_t q = ((qa0 + x0) * c1 + qa1 + x1) * c2 + qa2;
-    T* dst = cs + (x0 * S1 + x1) * S2;
-    for (int x2 = lane; x2 < n2; x2 += 32) dst[x2] = Z ? C[q + x2] - Z[q + x2] : C[q + x2];
+template <class T>
+struct ICfg {
+  static constexpr int NT = 512, NW = 16, NG = 2, WG = NW / NG;
+  static constexpr int TW2 = 64, TW1 = sizeof(T) == 8 ? 14 : 16;
+  static constexpr int NS = sizeof(T) == 8 ? 5 : 7;            // coefficient plane slots
+  static constexpr int V = 16 / int(sizeof(T));
+  static constexpr int ALN = 128 / int(sizeof(T));
+  static constexpr int FR = 2 * TW1, FC = 2 * TW2;             // fine rows / cols of a tile
+  static constexpr int NB = FR / 4;                            // bands of four fine rows
+  static_assert(NB <= WG, "one band per warp of a group");
+  static constexpr int BOX = (FC + V - 1 + V - 1) / V * V;     // aligned superset of a row
+  static constexpr int PITCH = (BOX + ALN - 1) / ALN * ALN;
+  static constexpr int SLOT = FR * PITCH;
+  static constexpr int CR = TW1 + 1, CC = TW2 + 1;             // coarse window
+  static constexpr int CBOX = (CC + V - 1 + V - 1) / V * V;
+  static constexpr int CPITCH = (CBOX + ALN - 1) / ALN * ALN;
+  static constexpr int CSLOT = CR * CPITCH;
+  static constexpr size_t c_off = size_t(NS) * SLOT * sizeof(T);  // [2 bufs][C, Z][CSLOT]
+  static constexpr size_t w_off = c_off + size_t(4) * CSLOT * sizeof(T);
+  static constexpr int W0N = kMaxSegI + 2;
+  static constexpr size_t bar_off = (w_off + size_t(2) * W0N * sizeof(T) + 15) / 16 * 16;
+  static constexpr size_t total = bar_off + (NS + 2) * sizeof(uint64_t);
+  static_assert(total <= 227 * 1024, "shared memory budget");
+};
+
+template <class T>
+struct Vec2i;
+template <>
+struct Vec2i<double> { using type = double2; };
+template <>
+struct Vec2i<float> { using type = float2; };
+
+// v[k] = row[pos + k], k < 2
+template <class T>
+__device__ __forceinline__ void ld2(const T* row, int pos, T& v0, T& v1) {
+  using T2 = typename Vec2i<T>::type;
+  if (!(pos & 1)) {
+    const T2 x = *reinterpret_cast<const T2*>(row + pos);
+    v0 = x.x;
+    v1 = x.y;
+  } else {
+    v0 = row[pos];
+    v1 = row[pos + 1];
   }
-  __syncthreads();
-  // owned fine ranges [2qa, min(2(qa+tb), e))
-  const int f0 = int(std::min<int64_t>(2 * (qa0 + tb0), e0) - 2 * qa0);
-  const int f1 = int(std::min<int64_t>(2 * (qa1 + tb1), e1) - 2 * qa1);
-  const int f2 = int(std::min<int64_t>(2 * (qa2 + tb2), e2) - 2 * qa2);
-  for (int x2 = tid; x2 < f2; x2 += NT) {
-    const int b = x2 >> 1;
-    const bool o2 = x2 & 1;
-    const int64_t i2 = 2 * qa2 + x2;
-    const T wl2 = o2 ? a.wl[2][i2 >> 1] : T(1), wr2 = o2 ? a.wr[2][i2 >> 1] : T(0);
-    const int bn = o2 ? b + 1 : b;
-    for (int x0 = 0; x0 < f0; ++x0) {
-      const bool o0 = x0 & 1;
-      const int64_t i0 = 2 * qa0 + x0;
-      const T w0l = o0 ? a.wl[0][i0 >> 1] : T(1), w0r = o0 ? a.wr[0][i0 >> 1] : T(0);
-      const T* pA = cs + (x0 >> 1) * S1 * S2;
-      const T* pB = o0 ? pA + S1 * S2 : pA;
-      // interpolant of the even fine row 2*q1 (dims 0 and 2)
-      auto reven = [&](int q1) {
-        const T vb = w0l * pA[q1 * S2 + b] + w0r * pB[q1 * S2 + b];
-        const T vn = w0l * pA[q1 * S2 + bn] + w0r * pB[q1 * S2 + bn];
-        return wl2 * vb + wr2 * vn;
-      };
-      const int64_t rowbase = (i0 * e1 + 2 * qa1) * e2 + i2;
-      T rcur = reven(0);
-#pragma unroll 4
-      for (int x1 = 0; x1 < f1; x1 += 2) {
-        const int64_t g0 = rowbase + int64_t(x1) * e2;
-        const bool has_odd = x1 + 1 < f1;
-        T cf0 = T(0), cf1 = T(0);
-        if (with) {
-          cf0 = coef[g0];
-          if (has_odd) cf1 = coef[g0 + e2];
-        }
-        const bool coarse = !(o0 | o2);  // even row x1: coarse node iff x0, x2 even
-        out[g0] = coarse ? rcur : cf0 + rcur;
-        if (has_odd) {
-          const int64_t i1 = 2 * qa1 + x1 + 1;
-          const T rnext = reven((x1 >> 1) + 1);
-          const T ip = a.wl[1][i1 >> 1] * rcur + a.wr[1][i1 >> 1] * rnext;
-          out[g0 + e2] = cf1 + ip;
-          rcur = rnext;
-        }
+}
+
+template <class T, bool WITH, bool HASZ>
+__global__ void __launch_bounds__(512, 1)
+    k_interp_march(const __grid_constant__ CUtensorMap mcoef, const __grid_constant__ CUtensorMap mC,
+                   const __grid_constant__ CUtensorMap mZ, int64_t coef_off, int64_t c_off,
+                   T* __restrict__ out, LevelArgs<T> a, int S0, int nt1, int nt2, int nseg,
+                   int seg_base) {
+  using C = ICfg<T>;
+  constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NW = C::NW;
+  constexpr int TW1 = C::TW1, TW2 = C::TW2, WG = C::WG, NB = C::NB;
+  constexpr int CPITCH = C::CPITCH, CSLOT = C::CSLOT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* ring = reinterpret_cast<T*>(smem);
+  T* cbuf = reinterpret_cast<T*>(smem + C::c_off);
+  T* w0t = reinterpret_cast<T*>(smem + C::w_off);  // [2][W0N] dim-0 weights of odd planes
+  uint64_t* barf = reinterpret_cast<uint64_t*>(smem + C::bar_off);
+  uint64_t* barc = barf + NS;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
+  const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
+  int bid = blockIdx.x;
+  const int t2i = bid % nt2;
+  bid /= nt2;
+  const int t1i = bid % nt1;
+  const int seg = seg_base + bid / nt1;
+  const bool lastseg = seg == nseg - 1;
+  const int64_t q1a = int64_t(t1i) * TW1, q2a = int64_t(t2i) * TW2;
+  const int tw1 = int(c1 - 1 - q1a < TW1 ? c1 - 1 - q1a : TW1);
+  const int tw2 = int(c2 - 1 - q2a < TW2 ? c2 - 1 - q2a : TW2);
+  const int64_t ka = int64_t(seg) * S0;
+  const int64_t kb = lastseg ? c0 - 1 : ka + S0;  // coarse planes ka..kb
+  const int64_t jlo = 2 * ka, jhi = lastseg ? e0 - 1 : 2 * kb - 1;  // owned fine planes
+  const int frows = 2 * tw1;
+
+  const int grp = warp / WG, wg = warp % WG;
+  const int t = 32 * grp + lane;  // tile-local coarse column
+  const int64_t tg = q2a + t;
+  const bool tvalid = t < tw2;
+  T hl = T(0), hr = T(0);
+  if (tvalid) {
+    hl = a.wl[2][tg];
+    hr = a.wr[2][tg];
+  }
+  const bool has_band = wg < NB;
+  const int b = 4 * wg;  // fine rows b..b+3 of the tile; coarse rows b/2 .. b/2+2
+  bool rown[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) rown[i] = has_band && tvalid && b + i < frows;
+  T w1l[2] = {T(0), T(0)}, w1r[2] = {T(0), T(0)};  // odd fine rows b+1, b+3
+  if (has_band) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int64_t gr = 2 * q1a + b + 1 + 2 * i;
+      if (gr < e1 - 1) { w1l[i] = a.wl[1][gr >> 1]; w1r[i] = a.wr[1][gr >> 1]; }
+    }
+  }
+
+  // ---- TMA: fine coefficient rows and coarse C / Z rows --------------------------------
+  const int64_t plane_f = e1 * e2, plane_c = c1 * c2;
+  const uint32_t tx_f = uint32_t(frows) * C::BOX * uint32_t(sizeof(T));
+  const int crows = tw1 + 1;
+  const uint32_t tx_c = uint32_t(crows) * C::CBOX * uint32_t(sizeof(T)) * (HASZ ? 2u : 1u);
+  auto issue_f = [&](int64_t j) {  // fine plane j into slot (j - jlo) % NS
+    const int sl = int(j - jlo) % NS;
+    if (tid == 0) ptx::mbar_arrive_expect_tx(&barf[sl], tx_f);
+    if (lane == 0) {
+      T* dst = ring + sl * SLOT;
+      const int64_t base = (j * e1 + 2 * q1a) * e2 + 2 * q2a - coef_off;
+      for (int r = warp; r < frows; r += NW) {
+        const int64_t f = base + int64_t(r) * e2;
+        ptx::tma_load_1d(dst + r * PITCH, &mcoef, int(f & ~int64_t(V - 1)), &barf[sl]);
       }
     }
+  };
+  auto issue_c = [&](int64_t m) {  // coarse plane m into buffer m & 1
+    const int bsl = int(m & 1);
+    if (tid == 0) ptx::mbar_arrive_expect_tx(&barc[bsl], tx_c);
+    if (lane == 0) {
+      T* dst = cbuf + bsl * 2 * CSLOT;
+      const int64_t base = (m * c1 + q1a) * c2 + q2a - c_off;
+      for (int r = warp; r < crows; r += NW) {
+        const int64_t f = base + int64_t(r) * c2;
+        const int x = int(f & ~int64_t(V - 1));
+        ptx::tma_load_1d(dst + r * CPITCH, &mC, x, &barc[bsl]);
+        if (HASZ) ptx::tma_load_1d(dst + CSLOT + r * CPITCH, &mZ, x, &barc[bsl]);
+      }
+    }
+  };
+
+  for (int i = tid; i < C::W0N; i += blockDim.x) {
+    const int64_t q = ka + i;  // dim-0 interval of odd plane 2q+1
+    const bool ok = e0 > 1 && q < c0 - 1;
+    w0t[i] = ok ? a.wl[0][q] : T(0);
+    w0t[C::W0N + i] = ok ? a.wr[0][q] : T(0);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < NS + 2; ++q) ptx::mbar_init(&barf[q], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (WITH)
+    for (int64_t j = jlo; j <= jhi && j < jlo + NS; ++j) issue_f(j);
+  issue_c(ka);
+  if (ka + 1 <= kb) issue_c(ka + 1);
+
+  const int e2m = int(e2 & (V - 1)), c2m = int(c2 & (V - 1));
+  const int fph0 = int((2 * q1a * e2 + 2 * q2a) & (V - 1));
+  const int cph0 = int((q1a * c2 + q2a) & (V - 1));
+  auto fpos = [&](int64_t j, int r) {
+    return int((j * plane_f + fph0 + int64_t(r) * e2m) & (V - 1)) + 2 * t;
+  };
+  auto cpos = [&](int64_t m, int s) {
+    return int((m * plane_c + cph0 + int64_t(s) * c2m) & (V - 1)) + t;
+  };
+
+  T A1p[4][2], A1[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) A1p[i][0] = A1p[i][1] = A1[i][0] = A1[i][1] = T(0);
+  T* obase = out + (2 * q1a + b) * e2 + 2 * q2a + 2 * t;
+
+  // one fine plane j: out = coef + interp (interp alone at coarse nodes / without coef)
+  auto fine_plane = [&](int64_t j, bool odd, T w0l, T w0r) {
+    const int p = int(j - jlo);
+    const T* S = ring + (p % NS) * SLOT;
+    if (WITH) ptx::mbar_wait(&barf[p % NS], uint32_t((p / NS) & 1));
+    if (!has_band) return;
+    T* o = obase + j * plane_f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      T ip0, ip1;
+      if (odd) {
+        ip0 = w0l * A1p[i][0] + w0r * A1[i][0];
+        ip1 = w0l * A1p[i][1] + w0r * A1[i][1];
+      } else {
+        ip0 = A1[i][0];
+        ip1 = A1[i][1];
+      }
+      T v0 = ip0, v1 = ip1;
+      if (WITH) {
+        T c0v, c1v;
+        ld2<T>(S + (b + i) * PITCH, fpos(j, b + i), c0v, c1v);
+        // the coarse node (even plane, even row, even column) keeps the interpolant
+        if (odd || (i & 1)) v0 += c0v;
+        v1 += c1v;
+      }
+      if (rown[i]) {
+        o[int64_t(i) * e2] = v0;
+        o[int64_t(i) * e2 + 1] = v1;
+      }
+    }
+  };
+
+  for (int64_t m = ka; m <= kb; ++m) {
+    // ---- coarse plane m: corrected window -> in-plane interpolant of fine plane 2m
+    const int bsl = int(m & 1);
+    ptx::mbar_wait(&barc[bsl], uint32_t(((m - ka) >> 1) & 1));
+    if (has_band) {
+      const T* Cb = cbuf + bsl * 2 * CSLOT;
+      T Cc[3][2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int s = b / 2 + k;
+        const int ps = cpos(m, s);
+        T x0, x1;
+        ld2<T>(Cb + s * CPITCH, ps, x0, x1);
+        if (HASZ) {
+          T z0, z1;
+          ld2<T>(Cb + CSLOT + s * CPITCH, ps, z0, z1);
+          x0 -= z0;
+          x1 -= z1;
+        }
+        Cc[k][0] = x0;
+        Cc[k][1] = x1;
+      }
+      T A2[3][2];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        A2[k][0] = Cc[k][0];
+        A2[k][1] = hl * Cc[k][0] + hr * Cc[k][1];
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        A1[0][c] = A2[0][c];
+        A1[1][c] = w1l[0] * A2[0][c] + w1r[0] * A2[1][c];
+        A1[2][c] = A2[1][c];
+        A1[3][c] = w1l[1] * A2[1][c] + w1r[1] * A2[2][c];
+      }
+    }
+    // ---- fine planes 2m-1 (odd) and 2m (even)
+    if (m > ka) {
+      const int iw = int(m - 1 - ka);
+      fine_plane(2 * m - 1, true, w0t[iw], w0t[C::W0N + iw]);
+    }
+    if (2 * m <= jhi) fine_plane(2 * m, false, T(0), T(0));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      A1p[i][0] = A1[i][0];
+      A1p[i][1] = A1[i][1];
+    }
+    __syncthreads();  // slots of planes 2m-1, 2m and coarse buffer m are free
+    if (WITH) {
+      if (m > ka && 2 * m - 1 + NS <= jhi) issue_f(2 * m - 1 + NS);
+      if (2 * m <= jhi && 2 * m + NS <= jhi) issue_f(2 * m + NS);
+    }
+    if (m + 2 <= kb) issue_c(m + 2);
+  }
+}
+
+// The last fine row (e1-1) and column (e2-1) of the level, every plane: one
+// thread per cell (reference-order multilinear interpolation, kernels.cuh).
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_interp_face(const T* coef, T* out, const T* __restrict__ C, const T* __restrict__ Z,
+                  LevelArgs<T> a, bool with) {
+  const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
+  const int64_t c1 = a.c[1], c2 = a.c[2];
+  const int64_t fA = e0 * e1, total = fA + e0 * (e2 - 1);
+  auto coarse = [&](int64_t q0, int64_t q1, int64_t q2) {
+    const int64_t q = (q0 * c1 + q1) * c2 + q2;
+    return Z ? C[q] - Z[q] : C[q];
+  };
+  for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < total;
+       it += int64_t(gridDim.x) * blockDim.x) {
+    int64_t j, r, c;
+    if (it < fA) {
+      j = it / e1; r = it % e1; c = e2 - 1;
+    } else {
+      const int64_t q = it - fA;
+      j = q / (e2 - 1); r = e1 - 1; c = q % (e2 - 1);
+    }
+    const int64_t idx = (j * e1 + r) * e2 + c;
+    if (((j | r | c) & 1) == 0) {
+      out[idx] = coarse(j >> 1, r >> 1, c >> 1);
+    } else {
+      const T ip = interp_node(a, j, r, c, coarse);
+      out[idx] = with ? coef[idx] + ip : ip;
+    }
+  }
+}
+
+template <class T, bool WITH, bool HASZ>
+void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs<T>& a,
+                cudaStream_t s) {
+  using Cf = ICfg<T>;
+  auto kern = k_interp_march<T, WITH, HASZ>;
+  static int attr_dev = -1;
+  int dev = 0;
+  HGR_CUDA_CHECK(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    HGR_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(Cf::total)));
+    attr_dev = dev;
+  }
+  const int nt1 = int((a.c[1] - 1 + Cf::TW1 - 1) / Cf::TW1);
+  const int nt2 = int((a.c[2] - 1 + Cf::TW2 - 1) / Cf::TW2);
+  const int64_t tiles = int64_t(nt1) * nt2;
+  int S0 = kMaxSegI;
+  while (S0 > 4 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
+  const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
+  constexpr int V = Cf::V;
+  const int64_t plane_f = a.e[1] * a.e[2], plane_c = a.c[1] * a.c[2];
+  const int64_t Nf = a.e[0] * plane_f, Nc = a.c[0] * plane_c;
+  const int64_t lim = (int64_t(1) << 31) - 4 * int64_t(Cf::BOX);
+  int sa = 0;
+  while (sa < nseg) {
+    // fine planes of segments sa..sb-1: [2*sa*S0, 2*(sb*S0) + 1]; coarse planes up to sb*S0 + 1
+    auto f_hi = [&](int sg) { return std::min<int64_t>(a.e[0] - 1, 2 * (int64_t(sg) + 1) * S0); };
+    const int64_t f_lo = 2 * int64_t(sa) * S0;
+    int sb = sa + 1;
+    while (sb < nseg && (f_hi(sb) + 1 - f_lo) * plane_f < lim) ++sb;
+    require((f_hi(sb - 1) + 1 - f_lo) * plane_f < lim, "level too large for the 1D TMA path");
+    const int64_t coef_off = (f_lo * plane_f) & ~int64_t(V - 1);
+    const int64_t c_off = ((int64_t(sa) * S0) * plane_c) & ~int64_t(V - 1);
+    CUtensorMap mcoef, mC, mZ;
+    make_tma_1d(&mC, Cv + c_off, uint64_t(Nc - c_off), int(sizeof(T)), Cf::CBOX);
+    mZ = mC;
+    if (HASZ) make_tma_1d(&mZ, Zv + c_off, uint64_t(Nc - c_off), int(sizeof(T)), Cf::CBOX);
+    mcoef = mC;
+    if (WITH) make_tma_1d(&mcoef, coef + coef_off, uint64_t(Nf - coef_off), int(sizeof(T)), Cf::BOX);
+    const int64_t blocks = tiles * (sb - sa);
+    kern<<<unsigned(blocks), Cf::NT, Cf::total, s>>>(mcoef, mC, mZ, coef_off, c_off, out, a, S0,
+                                                     nt1, nt2, nseg, sa);
+    HGR_CUDA_CHECK(cudaGetLastError());
+    sa = sb;
   }
 }
 
@@ -100,22 +367,16 @@ __global__ void __launch_bounds__(2 * B2) k_interp_rec(const T* coef, T* out, co
 template <class T>
 bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
                        bool with, cudaStream_t s) {
-  constexpr int B0 = 2, B1 = 16, B2 = 128;
-  const int64_t m0 = a.c[0] - 1, m1 = a.c[1] - 1, m2 = a.c[2] - 1;
-  const int nb0 = int(std::max<int64_t>(1, (m0 + B0 - 1) / B0));
-  const int nb1 = int(std::max<int64_t>(1, (m1 + B1 - 1) / B1));
-  const int nb2 = int(std::max<int64_t>(1, (m2 + B2 - 1) / B2));
-  const size_t smem = size_t(B0 + 1) * (B1 + 1) * (B2 + 2) * sizeof(T);
-  static int attr_dev = -1;
-  int dev = 0;
-  HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    HGR_CUDA_CHECK(cudaFuncSetAttribute(k_interp_rec<T, B0, B1, B2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_dev = dev;
-  }
-  k_interp_rec<T, B0, B1, B2><<<unsigned(int64_t(nb0) * nb1 * nb2), 2 * B2, smem, s>>>(
-      coef, out, C, Z, a, with, nb1, nb2);
+  const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (a.e[1] < 3 || a.e[2] < 3 || !al(C) || (Z && !al(Z)) || (with && !al(coef))) return false;
+  if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
+  if (a.c[0] * a.c[1] * a.c[2] >= (int64_t(1) << 31)) return false;
+  if (with && Z) run_interp<T, true, true>(coef, out, C, Z, a, s);
+  else if (with) run_interp<T, true, false>(coef, out, C, Z, a, s);
+  else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s);
+  else run_interp<T, false, false>(coef, out, C, Z, a, s);
+  const int64_t face = a.e[0] * (a.e[1] + a.e[2] - 1);
+  k_interp_face<T><<<grid_for(face, 256), 256, 0, s>>>(coef, out, C, Z, a, with);
   HGR_CUDA_CHECK(cudaGetLastError());
   return true;
 }
