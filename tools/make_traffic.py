@@ -1,0 +1,46 @@
+"""Build profiles/ncu_traffic.json (DRAM bytes per bench-bracket launch, per kernel class)
+from ncu launch lists of one warm round trip (tools/gpu_round.sh): the bench's roofline
+`traffic` field. usage: make_traffic.py CONFIG=launches.csv [CONFIG=launches.csv ...]"""
+import csv, io, json, re, sys, collections
+from pathlib import Path
+
+CLASSES = {  # bench kind -> (kernel-name regex, bench brackets per round trip)
+    "fused_decompose_level": (r"k_level_(fused|face)<\w+, 0>", None),
+    "fused_recompose_level": (r"k_level_(fused|face)<\w+, 2>", None),
+    "recompose_interp": (r"k_interp_(march|face)", None),
+    "thomas": (r"k_thomas_(lines|rows)", None),
+    "assembly": (r"k_scatter_even", None),
+}
+
+def per_trip(path):
+    lines = [l for l in open(path) if l.startswith('"')]
+    rows = list(csv.DictReader(io.StringIO(''.join(lines))))
+    agg = collections.OrderedDict()
+    for r in rows:
+        i = int(r['ID'])
+        name = r['Kernel Name'].split('(')[0].replace('void ', '').replace('(int)', '')
+        d = agg.setdefault(i, {'name': name})
+        d[r['Metric Name']] = float(r['Metric Value'].replace(',', ''))
+    ids = sorted(agg)
+    # the second (warm) round trip starts at the second decompose's first fused launch
+    dec = [i for i in ids if re.search(r"k_level_fused<\w+, 0>", agg[i]['name'])]
+    start = dec[len(dec) // 2]
+    return [agg[i] for i in ids if i >= start]
+
+out_path = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
+res = json.loads(out_path.read_text()) if out_path.exists() else {}
+for arg in sys.argv[1:]:
+    cfg, path = arg.split('=', 1)
+    launches = per_trip(path)
+    cls = {}
+    for kind, (rx, _) in CLASSES.items():
+        sel = [l for l in launches if re.search(rx, l['name'])]
+        main = [l for l in sel if not re.search(r"face", l['name'])]
+        if not main:
+            continue
+        tot = sum(l.get('dram__bytes_read.sum', 0) + l.get('dram__bytes_write.sum', 0) for l in sel)
+        # one bench bracket per main-kernel launch (faces share their level's bracket)
+        cls[kind] = round(tot / len(main))
+    res[cfg] = cls
+    print(cfg, cls)
+out_path.write_text(json.dumps(res, indent=1) + "\n")
