@@ -55,21 +55,28 @@ constexpr int kMaxSeg = 64;  // coarse planes per dim-0 segment (S0 <= kMaxSeg)
 
 template <class T>
 struct LCfg {
-  static constexpr int NT = 512, NW = NT / 32, NG = 2, WG = NW / NG;
-  static constexpr int TW2 = 64;                               // coarse columns (1 per lane)
+  // fp64: lane = 1 coarse column, 2 column groups, 16 warps, one CTA per SM;
+  // fp32: lane = 2 coarse columns (16-byte loads), 1 group, 8 warps, two CTAs per SM
+  static constexpr int CPL = sizeof(T) == 8 ? 1 : 2;           // coarse columns per lane
+  static constexpr int NG = 2 / CPL;                           // column groups
+  static constexpr int NT = sizeof(T) == 8 ? 512 : 256, NW = NT / 32, WG = NW / NG;
+  static constexpr int MINB = sizeof(T) == 8 ? 1 : 2;          // CTAs per SM
+  static constexpr int TW2 = 64;                               // coarse columns
   static constexpr int TW1 = sizeof(T) == 8 ? 14 : 16;         // coarse rows
-  static constexpr int NS = sizeof(T) == 8 ? 5 : 8;            // ring slots
+  static constexpr int NS = sizeof(T) == 8 ? 5 : 4;            // ring slots
   static constexpr int V = 16 / int(sizeof(T));                // elements per 16 bytes
   static constexpr int RW = 2 * TW1 + 3, CW = 2 * TW2 + 3;     // window rows / columns
   static constexpr int NB = TW1 / 2;                           // bands of 4 owned rows
   static_assert(NB <= WG, "one band per warp of a group");
+  static constexpr int NCELL = 2 * CPL, NV = 2 * CPL + 3;      // cells / window values per lane
   static constexpr int BOX = (CW + V - 1 + V - 1) / V * V;     // aligned superset of a row
   static constexpr int ALN = 128 / int(sizeof(T));             // TMA smem alignment (128 B)
   static constexpr int PITCH = (BOX + ALN - 1) / ALN * ALN;
-  static_assert(PITCH >= CW + V, "reads stay inside the row");
+  static_assert(PITCH >= CW + 2 * V, "vector reads stay inside the row");
   static constexpr int SLOT = RW * PITCH;
   static constexpr int P2W = TW2;
-  static constexpr int NQ = TW1 * (TW2 / 2);                   // column-stage work items
+  static constexpr int CQ = V;                                 // column-stage columns per item
+  static constexpr int NQ = TW1 * (TW2 / CQ);                  // column-stage work items
   static_assert(NQ <= NT, "one column-stage item per thread");
   static constexpr int K0N = kMaxSeg + 6;                      // K0 tap rows ka-2 .. kb+1
   static constexpr int W0N = kMaxSeg + 4;                      // dim-0 weights ka-1 .. kb+2
@@ -79,7 +86,7 @@ struct LCfg {
   static constexpr size_t w0_off = k0_off + size_t(K0N) * 5 * sizeof(T);
   static constexpr size_t bar_off = (w0_off + size_t(2) * W0N * sizeof(T) + 15) / 16 * 16;
   static constexpr size_t total = bar_off + NS * sizeof(uint64_t);
-  static_assert(total <= 227 * 1024, "shared memory budget");
+  static_assert(total * MINB <= 227 * 1024, "shared memory budget");
 };
 
 template <class T>
@@ -103,19 +110,37 @@ __device__ __forceinline__ void load5(const T* row, int pos, T (&v)[5]) {
     v[0] = row[pos]; v[1] = x.x; v[2] = x.y; v[3] = y.x; v[4] = y.y;
   }
 }
-template <class T>
-__device__ __forceinline__ void load2(const T* row, int pos, T (&v)[2]) {
-  using T2 = typename Vec2<T>::type;
-  if (!(pos & 1)) {
-    const T2 x = *reinterpret_cast<const T2*>(row + pos);
-    v[0] = x.x; v[1] = x.y;
+// fp32: v[k] = row[base + ph + k], k < 7, base a multiple of 4 (16-byte float4 loads)
+template <int PH>
+__device__ __forceinline__ void load7f(const float* row, int base, float (&v)[7]) {
+  const float4* p = reinterpret_cast<const float4*>(row + base);
+  const float4 a = p[0], b = p[1];
+  float w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, 0.f, 0.f, 0.f, 0.f};
+  if constexpr (PH >= 2) {
+    const float4 c = p[2];
+    w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+  }
+#pragma unroll
+  for (int k = 0; k < 7; ++k) v[k] = w[k + PH];
+}
+// the lane's window values: NV = 2*CPL+3 values starting at window column base
+template <class T, int NV>
+__device__ __forceinline__ void loadV(const T* row, int ph, int base, T (&v)[NV]) {
+  if constexpr (NV == 5) {
+    load5<T>(row, ph + base, v);
   } else {
-    v[0] = row[pos]; v[1] = row[pos + 1];
+    static_assert(NV == 7 && sizeof(T) == 4, "fp32 lanes own two coarse columns");
+    switch (ph) {
+      case 0: load7f<0>(row, base, v); break;
+      case 1: load7f<1>(row, base, v); break;
+      case 2: load7f<2>(row, base, v); break;
+      default: load7f<3>(row, base, v); break;
+    }
   }
 }
 
 template <class T, int MODE>
-__global__ void __launch_bounds__(LCfg<T>::NT, 1)
+__global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
     k_level_fused(const __grid_constant__ CUtensorMap map, int64_t map_off, T* __restrict__ coef_out,
                   T* __restrict__ zload, T* __restrict__ gather, LevelArgs<T> a, int S0, int nt1,
                   int nt2, int nseg, int seg_base, int* flag) {
@@ -123,6 +148,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
   using T2 = typename Vec2<T>::type;
   constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NT = C::NT;
   constexpr int TW1 = C::TW1, TW2 = C::TW2, P2W = C::P2W, NW = C::NW, NB = C::NB, WG = C::WG;
+  constexpr int CPL = C::CPL, NCELL = C::NCELL, NV = C::NV, CQ = C::CQ;
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
   extern __shared__ __align__(128) unsigned char smem[];
   T* raw = reinterpret_cast<T*>(smem);
@@ -154,18 +180,21 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
   const int64_t jend = (2 * kb) < (e0 - 1) ? (2 * kb) : (e0 - 1);
   const int orows = 2 * tw1;  // owned fine rows: window rows [2, 2 + orows)
 
-  // ---- per-lane column: coarse column t (tile-local), window columns 2t..2t+4 --------
+  // ---- per-lane columns: coarse t0..t0+CPL-1 (tile-local), window columns 2t0.. -------
   const int grp = warp / WG, wg = warp % WG;
-  const int t = 32 * grp + lane;
-  const int64_t tg = q2a + t;  // global coarse column
-  const bool tvalid = t < tw2;
-  T k2[5];
+  const int t0 = CPL * (32 * grp + lane);
+  const int wb = 2 * t0;  // first window column of the lane
+  T k2[CPL][5];
+  T hl[CPL], hr[CPL];  // interpolation weights of the odd cells 2t+3
+  bool cvalid[CPL];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) k2[k] = tvalid ? a.taps[2][tg * 5 + k] : T(0);
-  T hl = T(0), hr = T(0);  // interpolation weights of cell 2t+3 (odd column)
-  if (DEC && tvalid) {
-    hl = a.wl[2][tg];
-    hr = a.wr[2][tg];
+  for (int c = 0; c < CPL; ++c) {
+    const int64_t tg = q2a + t0 + c;
+    cvalid[c] = t0 + c < tw2;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) k2[c][k] = cvalid[c] ? a.taps[2][tg * 5 + k] : T(0);
+    hl[c] = (DEC && cvalid[c]) ? a.wl[2][tg] : T(0);
+    hr[c] = (DEC && cvalid[c]) ? a.wr[2][tg] : T(0);
   }
 
   // ---- per-warp row band: owned rows [b, b+4), lookahead row b+4 ---------------------
@@ -173,7 +202,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
   const int b = 2 + 4 * wg;
   bool rown[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) rown[i] = has_band && b + i - 2 < orows && tvalid;
+  for (int i = 0; i < 4; ++i) rown[i] = has_band && b + i - 2 < orows;
   T w1l[2] = {T(0), T(0)}, w1r[2] = {T(0), T(0)};  // odd rows b+1, b+3
   if (DEC && has_band) {
 #pragma unroll
@@ -182,15 +211,15 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
       if (gr < e1 - 1) { w1l[i] = a.wl[1][gr >> 1]; w1r[i] = a.wr[1][gr >> 1]; }
     }
   }
-  // K-only rows outside the bands: window rows 0, 1 (and the last window row is the
+  // K-only rows outside the bands: window rows 0, 1 (the last window row is the
   // lookahead row of the last band)
   const int xr0 = (wg == WG - 1) ? 0 : -1;
   const int xr1 = (NB < WG) ? ((wg == WG - 1) ? 1 : -1) : ((wg == WG - 2) ? 1 : -1);
   const bool krow_look = wg == NB - 1;
 
-  // ---- column stage item: coarse row s, columns cq, cq+1 ------------------------------
+  // ---- column stage item: coarse row s, columns cq..cq+CQ-1 ---------------------------
   const bool qv = tid < C::NQ;
-  const int s = tid / (TW2 / 2), cq = 2 * (tid % (TW2 / 2));
+  const int s = tid / (TW2 / CQ), cq = CQ * (tid % (TW2 / CQ));
   T k1[5];
 #pragma unroll
   for (int k = 0; k < 5; ++k) k1[k] = (qv && s < tw1) ? a.taps[1][(q1a + s) * 5 + k] : T(0);
@@ -200,9 +229,9 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
   for (int r = 0; r < RWn; ++r) nrows_in += (wr0 + r >= 0 && wr0 + r < e1) ? 1 : 0;
   const uint32_t tx_bytes = uint32_t(nrows_in) * C::BOX * uint32_t(sizeof(T));
   // per issuing lane (lane 0 of warp w: rows w, w+NW, ...): 32-bit TMA coordinate of
-  // window column 0 of the row in plane 0 (relative to the map base)
+  // window column 0 of the row in plane 0 relative to the map base (arithmetic
+  // modulo 2^32: the true coordinates of a launch lie in [-2, 2^31))
   constexpr int RPW = (C::RW + NW - 1) / NW;
-  // (arithmetic modulo 2^32: the true coordinates of a launch lie in [-2, 2^31))
   uint32_t rc[RPW];
   unsigned rvalid = 0;
 #pragma unroll
@@ -253,33 +282,62 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
 
   const int e2m = int(e2 & (V - 1));
   const int ph00 = int((wr0 * e2 + wc0) & (V - 1));
-  // shared-memory position of window column 2t in row r of a plane with phase phj
+  // phase (shared-memory position of window column 0) of row r in a plane of phase phj
   auto plane_ph = [&](int64_t jj) { return int((jj * plane_sz + ph00) & (V - 1)); };
-  auto pos = [&](int phj, int r) { return ((phj + r * e2m) & (V - 1)) + 2 * t; };
+  auto rph = [&](int phj, int r) { return (phj + r * e2m) & (V - 1); };
 
-  T acc0[2], acc1[2], acc2[2];
+  T acc0[CQ], acc1[CQ], acc2[CQ];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) acc0[k] = acc1[k] = acc2[k] = T(0);
-  T A1p[4][2];  // interpolant of the previous even plane at this lane's band cells
+  for (int k = 0; k < CQ; ++k) acc0[k] = acc1[k] = acc2[k] = T(0);
+  T A1p[4][NCELL];  // interpolant of the previous even plane at this lane's band cells
 #pragma unroll
-  for (int i = 0; i < 4; ++i) A1p[i][0] = A1p[i][1] = T(0);
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < NCELL; ++k) A1p[i][k] = T(0);
   T bad = T(0);
 
-  auto k2dot = [&](const T (&v)[5], bool masked) {
-    if (REC && masked) return k2[1] * v[1] + k2[3] * v[3];
-    return (k2[0] * v[0] + k2[1] * v[1] + k2[2] * v[2]) + (k2[3] * v[3] + k2[4] * v[4]);
+  // K2 of one row at the lane's coarse columns -> P2 row
+  auto k2row = [&](const T (&v)[NV], bool masked, T* P2row) {
+    T pv[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const T* u = v + 2 * c;
+      if (REC && masked)
+        pv[c] = k2[c][1] * u[1] + k2[c][3] * u[3];
+      else
+        pv[c] = (k2[c][0] * u[0] + k2[c][1] * u[1] + k2[c][2] * u[2]) +
+                (k2[c][3] * u[3] + k2[c][4] * u[4]);
+    }
+    if constexpr (CPL == 1) {
+      P2row[t0] = pv[0];
+    } else {
+      T2 w;
+      w.x = pv[0];
+      w.y = pv[1];
+      *reinterpret_cast<T2*>(P2row + t0) = w;
+    }
   };
 
   // column stage for plane jj: K1 over the P2 rows, K0 into the accumulators
   auto column_stage = [&](int64_t jj) {
     if (!qv) return;
     const T* P2 = p2 + (jj & 1) * (C::RW * P2W) + 2 * s * P2W + cq;
-    T P0 = T(0), P1 = T(0);
+    T P[CQ];
+#pragma unroll
+    for (int k = 0; k < CQ; ++k) P[k] = T(0);
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
-      const T2 x = *reinterpret_cast<const T2*>(P2 + k * P2W);
-      P0 += k1[k] * x.x;
-      P1 += k1[k] * x.y;
+      if constexpr (CQ == 2) {
+        const T2 x = *reinterpret_cast<const T2*>(P2 + k * P2W);
+        P[0] += k1[k] * x.x;
+        P[1] += k1[k] * x.y;
+      } else {
+        const float4 x = *reinterpret_cast<const float4*>(P2 + k * P2W);
+        P[0] += k1[k] * x.x;
+        P[1] += k1[k] * x.y;
+        P[2] += k1[k] * x.z;
+        P[3] += k1[k] * x.w;
+      }
     }
     const int64_t E = (jj & 1) ? jj + 1 : jj;
     const int ib0 = int(E / 2 - 1 - (ka - 2));  // K0 table row of coarse plane E/2 - 1
@@ -293,19 +351,23 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
       kB = k0t[(ib0 + 1) * 5 + 1];
       kC = T(0);
     }
-    acc0[0] += kA * P0; acc0[1] += kA * P1;
-    acc1[0] += kB * P0; acc1[1] += kB * P1;
-    acc2[0] += kC * P0; acc2[1] += kC * P1;
+#pragma unroll
+    for (int k = 0; k < CQ; ++k) {
+      acc0[k] += kA * P[k];
+      acc1[k] += kB * P[k];
+      acc2[k] += kC * P[k];
+    }
   };
   // store coarse plane i (acc0) if this segment owns it, then rotate
   auto flush = [&](int64_t i) {
     if (qv && i >= ka && i < kb && s < tw1) {
       T* zr = zload + (i * c1 + q1a + s) * c2 + q2a + cq;
-      if (cq < tw2) zr[0] = acc0[0];
-      if (cq + 1 < tw2) zr[1] = acc0[1];
+#pragma unroll
+      for (int k = 0; k < CQ; ++k)
+        if (cq + k < tw2) zr[k] = acc0[k];
     }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < CQ; ++k) {
       acc0[k] = acc1[k];
       acc1[k] = acc2[k];
       acc2[k] = T(0);
@@ -317,18 +379,18 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
     const int sl = p % NS;
     ptx::mbar_wait(&bar[sl], uint32_t((p / NS) & 1));
     const T* S = raw + sl * SLOT;
-    T* P2 = p2 + (j & 1) * (C::RW * P2W) + t;
+    T* P2 = p2 + (j & 1) * (C::RW * P2W);
     const bool jodd = j & 1;
-    const int phj = plane_ph(j), phm = plane_ph(j - 1);
+    const int phj = plane_ph(j);
 
     // ---- row stage ----
 #pragma unroll
     for (int xi = 0; xi < 2; ++xi) {  // K-only rows 0, 1
       const int xr = xi ? xr1 : xr0;
       if (xr >= 0) {
-        T v[5];
-        load5<T>(S + xr * PITCH, pos(phj, xr), v);
-        P2[xr * P2W] = k2dot(v, !jodd && !(xr & 1));
+        T v[NV];
+        loadV<T, NV>(S + xr * PITCH, rph(phj, xr), wb, v);
+        k2row(v, !jodd && !(xr & 1), P2 + xr * P2W);
       }
     }
     if (has_band) {
@@ -338,12 +400,17 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
         for (int i = 0; i < 5; ++i) {
           const int r = b + i;
           if (i == 4 && !krow_look) break;
-          T v[5];
-          load5<T>(S + r * PITCH, pos(phj, r), v);
+          T v[NV];
+          loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
           const bool masked = !jodd && !(r & 1);
-          P2[r * P2W] = k2dot(v, masked);
-          if (REC && masked && i < 4 && rown[i] && j >= 2 * ka && j < 2 * kb)
-            gather[((j >> 1) * c1 + ((wr0 + r) >> 1)) * c2 + tg] = v[2];  // coarse node -> C_{l-1}
+          k2row(v, masked, P2 + r * P2W);
+          if (REC && masked && i < 4 && rown[i] && j >= 2 * ka && j < 2 * kb) {
+            // gather the coarse nodes of this row into C_{l-1}
+            T* gd = gather + ((j >> 1) * c1 + ((wr0 + r) >> 1)) * c2 + q2a + t0;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+              if (cvalid[c]) gd[c] = v[2 + 2 * c];
+          }
         }
       } else {
         // decompose, even plane j: K path, coefficients of j and of the odd
@@ -353,50 +420,55 @@ __global__ void __launch_bounds__(LCfg<T>::NT, 1)
         const int iw = int(((j - 1) >> 1) - (ka - 1));
         const T w0l = own_o ? w0t[iw] : T(0), w0r = own_o ? w0t[C::W0N + iw] : T(0);
         const T* So = raw + ((p + NS - 1) % NS) * SLOT;  // slot of plane j-1
-        T* orow_e = coef_out + (j * e1 + wr0 + b) * e2 + wc0 + 2 * t + 2;
+        const int phm = plane_ph(j - 1);
+        T* orow_e = coef_out + (j * e1 + wr0 + b) * e2 + wc0 + wb + 2;
         T* orow_o = orow_e - plane_sz;
-        T A2e[3][2];  // dim-2 interpolants of the even rows b, b+2, b+4
+        T A2e[3][NCELL];  // dim-2 interpolants of the even rows b, b+2, b+4
         // row order b, b+2, b+1, b+4, b+3: odd rows see both even neighbours
 #pragma unroll
         for (int step = 0; step < 5; ++step) {
           const int i = step == 0 ? 0 : step == 1 ? 2 : step == 2 ? 1 : step == 3 ? 4 : 3;
           const int r = b + i;
-          T v[5];
-          load5<T>(S + r * PITCH, pos(phj, r), v);
-          if (i < 4 || krow_look) P2[r * P2W] = k2dot(v, false);
+          T v[NV];
+          loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
+          if (i < 4 || krow_look) k2row(v, false, P2 + r * P2W);
           if (!(i & 1)) {
-            A2e[i >> 1][0] = v[2];
-            A2e[i >> 1][1] = hl * v[2] + hr * v[4];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+              A2e[i >> 1][2 * c] = v[2 + 2 * c];
+              A2e[i >> 1][2 * c + 1] = hl[c] * v[2 + 2 * c] + hr[c] * v[4 + 2 * c];
+            }
           }
           if (i == 4) continue;
-          T A1[2];
+          T A1[NCELL];
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
+          for (int k = 0; k < NCELL; ++k)
             A1[k] = (i & 1) ? w1l[i >> 1] * A2e[i >> 1][k] + w1r[i >> 1] * A2e[(i >> 1) + 1][k]
                             : A2e[i >> 1][k];
           if (rown[i]) {
             if (own_e) {
-              const T c0v = v[2] - A1[0], c1v = v[3] - A1[1];
-              bad = c0v * T(0) + bad;
-              bad = c1v * T(0) + bad;
               T* o = orow_e + int64_t(i) * e2;
-              o[0] = c0v;
-              o[1] = c1v;
+#pragma unroll
+              for (int k = 0; k < NCELL; ++k) {
+                const T cv = v[2 + k] - A1[k];
+                bad = cv * T(0) + bad;
+                if (cvalid[k >> 1]) o[k] = cv;
+              }
             }
             if (own_o) {
-              T u[2];
-              load2<T>(So + r * PITCH, pos(phm, r) + 2, u);
-              const T c0v = u[0] - (w0l * A1p[i][0] + w0r * A1[0]);
-              const T c1v = u[1] - (w0l * A1p[i][1] + w0r * A1[1]);
-              bad = c0v * T(0) + bad;
-              bad = c1v * T(0) + bad;
+              T u[NV];
+              loadV<T, NV>(So + r * PITCH, rph(phm, r), wb, u);
               T* o = orow_o + int64_t(i) * e2;
-              o[0] = c0v;
-              o[1] = c1v;
+#pragma unroll
+              for (int k = 0; k < NCELL; ++k) {
+                const T cv = u[2 + k] - (w0l * A1p[i][k] + w0r * A1[k]);
+                bad = cv * T(0) + bad;
+                if (cvalid[k >> 1]) o[k] = cv;
+              }
             }
           }
-          A1p[i][0] = A1[0];
-          A1p[i][1] = A1[1];
+#pragma unroll
+          for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[k];
         }
       }
     }
