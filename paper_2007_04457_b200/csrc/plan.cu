@@ -72,6 +72,11 @@ int Plan::sync_status(cudaStream_t s) {
 }
 
 Plan::~Plan() {
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (gstream_) cudaStreamDestroy(gstream_);
+  for (cudaEvent_t e : gev_)
+    if (e) cudaEventDestroy(e);
   for (auto& r : prof_pending_) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -123,6 +128,58 @@ void Plan::read_profile(KindStats out[kKindCount]) {
   }
   prof_pending_.clear();
   for (int i = 0; i < kKindCount; ++i) out[i] = prof_acc_[i];
+}
+
+void Plan::run_graphed(int dir, const void* in, const void* out, int m, cudaStream_t s,
+                       const std::function<void(cudaStream_t)>& direct) {
+  if (profiling_ || !use_graphs) {
+    direct(s);
+    return;
+  }
+  ++graph_clock_;
+  GraphEntry* e = nullptr;
+  for (auto& g : graphs_)
+    if (g.dir == dir && g.in == in && g.out == out && g.m == m) e = &g;
+  if (!e) {  // first sighting: run directly, capture next time
+    if (graphs_.size() >= 8) {
+      auto lru = std::min_element(graphs_.begin(), graphs_.end(), [](const GraphEntry& a,
+                                                                     const GraphEntry& b) {
+        return a.last_use < b.last_use;
+      });
+      if (lru->exec) cudaGraphExecDestroy(lru->exec);
+      graphs_.erase(lru);
+    }
+    graphs_.push_back(GraphEntry{dir, in, out, m, nullptr, graph_clock_});
+    direct(s);
+    return;
+  }
+  e->last_use = graph_clock_;
+  if (!gstream_) {
+    HGR_CUDA_CHECK(cudaStreamCreateWithFlags(&gstream_, cudaStreamNonBlocking));
+    HGR_CUDA_CHECK(cudaEventCreateWithFlags(&gev_[0], cudaEventDisableTiming));
+    HGR_CUDA_CHECK(cudaEventCreateWithFlags(&gev_[1], cudaEventDisableTiming));
+  }
+  if (!e->exec) {
+    HGR_CUDA_CHECK(cudaStreamBeginCapture(gstream_, cudaStreamCaptureModeThreadLocal));
+    try {
+      direct(gstream_);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(gstream_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    HGR_CUDA_CHECK(cudaStreamEndCapture(gstream_, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&e->exec, g, 0);
+    cudaGraphDestroy(g);
+    HGR_CUDA_CHECK(ie);
+  }
+  HGR_CUDA_CHECK(cudaEventRecord(gev_[0], s));
+  HGR_CUDA_CHECK(cudaStreamWaitEvent(gstream_, gev_[0], 0));
+  HGR_CUDA_CHECK(cudaGraphLaunch(e->exec, gstream_));
+  HGR_CUDA_CHECK(cudaEventRecord(gev_[1], gstream_));
+  HGR_CUDA_CHECK(cudaStreamWaitEvent(s, gev_[1], 0));
 }
 
 // ---- precision-specific plan ----------------------------------------------------
@@ -212,6 +269,8 @@ class PlanT final : public Plan {
   void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) override;
 
   void decompose_to(const void* d_in, void* d_out, cudaStream_t s) override;
+  void decompose_to_direct(const void* d_in, void* d_out, cudaStream_t s);
+  void recompose_direct(const void* d_in, void* d_out, int upto, cudaStream_t s);
 
  private:
   void correction(int l, const T* in, T* z, T* apply, int sign, cudaStream_t s);
@@ -504,6 +563,11 @@ void PlanT<T>::assemble(T* out, cudaStream_t s) {
 template <class T>
 void PlanT<T>::decompose_to(const void* d_in, void* d_out, cudaStream_t s) {
   if (d_in == d_out) return decompose(d_out, s);
+  run_graphed(0, d_in, d_out, 0, s, [&](cudaStream_t st) { decompose_to_direct(d_in, d_out, st); });
+}
+
+template <class T>
+void PlanT<T>::decompose_to_direct(const void* d_in, void* d_out, cudaStream_t s) {
   const T* in = static_cast<const T*>(d_in);
   T* out = static_cast<T*>(d_out);
   launch_count_ = 0;
@@ -546,6 +610,12 @@ void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
 // applies coarse -= z_l and the interpolation (refined = coef + interp).
 template <class T>
 void PlanT<T>::recompose(const void* d_in, void* d_out, int m, cudaStream_t s) {
+  require(m >= 0 && m <= L(), "recompose: class index out of range");
+  run_graphed(1, d_in, d_out, m, s, [&](cudaStream_t st) { recompose_direct(d_in, d_out, m, st); });
+}
+
+template <class T>
+void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream_t s) {
   const T* in = static_cast<const T*>(d_in);
   T* out = static_cast<T*>(d_out);
   launch_count_ = 0;

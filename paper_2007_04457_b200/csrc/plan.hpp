@@ -10,6 +10,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -104,6 +105,29 @@ class Plan {
   std::vector<cudaEvent_t> ev_free_;
   KindStats prof_acc_[kKindCount];
   cudaEvent_t take_event();
+
+  // CUDA-graph replay of whole decompose / recompose launch sequences, keyed by
+  // (direction, input, output, prefix): the first call runs directly (it also
+  // sets kernel attributes), the second captures the sequence on a private
+  // stream and every call from then on replays it, ordered after / before the
+  // caller's stream by events. Disabled while profiling (per-launch events).
+  void run_graphed(int dir, const void* in, const void* out, int m, cudaStream_t s,
+                   const std::function<void(cudaStream_t)>& direct);
+  struct GraphEntry {
+    int dir;
+    const void* in;
+    const void* out;
+    int m;
+    cudaGraphExec_t exec;
+    unsigned long last_use;
+  };
+  std::vector<GraphEntry> graphs_;
+  unsigned long graph_clock_ = 0;
+  cudaStream_t gstream_ = nullptr;
+  cudaEvent_t gev_[2] = {nullptr, nullptr};
+
+ public:
+  bool use_graphs = true;
 };
 
 std::unique_ptr<Plan> make_plan(const hgr_grid_desc* g, int dtype);
