@@ -22,6 +22,8 @@
 //     contiguous block moved by one bulk copy (TMA engine) into a double-buffered
 //     shared-memory tile; each row is cut into 16*32/R chunks spread over the
 //     lanes; results go back through the tile and one bulk store.
+#include <type_traits>
+
 #include "kernels_fused.cuh"
 #include "plan.hpp"
 #include "ptx.cuh"
@@ -60,9 +62,48 @@ __device__ void build_tables(T* tm, T* tP, T* tp, T* tu, T* tQ, int n, int NC, i
   __syncthreads();
 }
 
-template <class T, int CH>
+// chunk solves of LPT lines at once (the line-independent table values are
+// loaded once for all of them)
+template <class T, int CH, int LPT = 1>
 struct ChunkSolve {
-  // forward local (zero carry) in place; returns the chunk's last value
+  // forward local (zero carry) in place; g[u] = the chunk's last value of line u
+  static __device__ __forceinline__ void fwd_local(T (&x)[LPT][CH], const T* tm, T (&g)[LPT]) {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) g[u] = T(0);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const T m = tm[k];
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) {
+        g[u] = x[u][k] - m * g[u];
+        x[u][k] = g[u];
+      }
+    }
+  }
+  static __device__ __forceinline__ void apply(T (&x)[LPT][CH], const T* tab, const T (&c)[LPT]) {
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const T t = tab[k];
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) x[u][k] += t * c[u];
+    }
+  }
+  // backward local (zero carry) in place; h[u] = the chunk's first value of line u
+  static __device__ __forceinline__ void bwd_local(T (&x)[LPT][CH], const T* tu, const T* tp,
+                                                   T (&h)[LPT]) {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) h[u] = T(0);
+#pragma unroll
+    for (int k = CH - 1; k >= 0; --k) {
+      const T uu = tu[k], pp = tp[k];
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) {
+        h[u] = (x[u][k] - uu * h[u]) * pp;
+        x[u][k] = h[u];
+      }
+    }
+  }
+  // single-line convenience forms
   static __device__ __forceinline__ T fwd_local(T (&x)[CH], const T* tm) {
     T g = T(0);
 #pragma unroll
@@ -76,7 +117,6 @@ struct ChunkSolve {
 #pragma unroll
     for (int k = 0; k < CH; ++k) x[k] += tab[k] * c;
   }
-  // backward local (zero carry) in place; returns the chunk's first value
   static __device__ __forceinline__ T bwd_local(T (&x)[CH], const T* tu, const T* tp) {
     T h = T(0);
 #pragma unroll
@@ -92,82 +132,159 @@ struct ChunkSolve {
 
 constexpr int kLW = 16;  // warps (= chunks per line) of k_thomas_lines
 
-// Groups: "full" groups (ia, ib) cover lines ib*32 .. ib*32+31 along dim 2 of
-// row ia of the other strided dim; when c2 % 32 != 0 the remaining columns
-// form "tail" groups whose lanes take 32 consecutive ia at one column. All
-// offsets are 32-bit (the launcher requires < 2^31 elements).
-template <class T, int CH>
+// Groups: "full" groups (ia, ib) cover lines ib*W .. ib*W+W-1 (W = 32*LPT; lane
+// L owns the LPT adjacent lines W*ib + LPT*L + u) along dim 2 of row ia of the
+// other strided dim; the c2 % W remaining columns form "tail" groups whose
+// threads take W consecutive ia at one column. All offsets are 32-bit (the
+// launcher requires < 2^31 elements).
+template <class T, int CH, int LPT, bool RP>
 __global__ void __launch_bounds__(32 * kLW, 1)
     k_thomas_lines(const T* in, T* out, int n, int sd, int so, int na, int c2, int nfull,
                    int ntail, int ngroups, const T* __restrict__ mult, const T* __restrict__ rpiv,
                    const T* __restrict__ upper) {
-  constexpr int NT = 32 * kLW, NC = kLW, NP = NC * CH;
+  constexpr int NT = 32 * kLW, NC = kLW, NP = NC * CH, GW = 32 * LPT;
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
   T* tP = tm + NP;
   T* tp = tP + NP;
   T* tu = tp + NP;
   T* tQ = tu + NP;
-  T* sf = tQ + NP;         // [NC][32] forward chunk summaries
-  T* sb = sf + NC * 32;    // [NC][32] backward chunk summaries
-  T* land = sb + NC * 32;  // [CH][NT] per-thread landing zone
+  T* sf = tQ + NP;         // [NC][GW] forward chunk summaries
+  T* sb = sf + NC * GW;    // [NC][GW] backward chunk summaries
+  T* land = sb + NC * GW;  // [CH][NT][LPT] per-thread landing zone
   build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s0 = w * CH;
   const int kmax = n - s0 < CH ? n - s0 : CH;  // valid positions of this warp's chunk
   const int nfull_groups = na * nfull;
 
-  // element offset of position s0 of this lane's line in group g (-1: no line)
-  auto line_off = [&](int g) {
+  // offset of position s0 of line u of this thread in group g (-1: no line);
+  // full groups: lines adjacent (offset + u), tail groups: offset + u*so
+  auto line_off = [&](int g, int u) {
     if (g < nfull_groups) {
       const int ia = int(unsigned(g) / unsigned(nfull)), ib = g - ia * nfull;
-      return ia * so + ib * 32 + lane + s0 * sd;
+      return ia * so + ib * GW + LPT * lane + u + s0 * sd;
     }
-    const int t = g - nfull_groups;  // tail: 32 rows ia at column c2 - ntail + (t % ntail)
-    const int ia = (t / ntail) * 32 + lane, col = c2 - ntail + t % ntail;
+    const int t = g - nfull_groups;  // tail: GW rows ia at column c2 - ntail + (t % ntail)
+    const int ia = (t / ntail) * GW + LPT * lane + u, col = c2 - ntail + t % ntail;
     return ia < na ? ia * so + col + s0 * sd : -1;
   };
   auto prefetch = [&](int g) {
-    const int off = line_off(g);
-    const T* src = in + (off < 0 ? 0 : off);
+    T* ld = land + tid * LPT;
+    if (g < nfull_groups) {
+      const T* src = in + line_off(g, 0);
 #pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      const bool ok = off >= 0 && k < kmax;
-      ptx::cp_async_elem<int(sizeof(T))>(land + k * NT + tid, src, ok ? int(sizeof(T)) : 0);
-      if (k + 1 < kmax) src += sd;
+      for (int k = 0; k < CH; ++k) {
+        const int by = k < kmax ? int(sizeof(T)) : 0;
+#pragma unroll
+        for (int u = 0; u < LPT; ++u)
+          ptx::cp_async_elem<int(sizeof(T))>(ld + k * NT * LPT + u, src + u, by);
+        if (k + 1 < kmax) src += sd;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) {
+        const int off = line_off(g, u);
+        const T* src = in + (off < 0 ? 0 : off);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const bool ok = off >= 0 && k < kmax;
+          ptx::cp_async_elem<int(sizeof(T))>(ld + k * NT * LPT + u, src, ok ? int(sizeof(T)) : 0);
+          if (k + 1 < kmax) src += sd;
+        }
+      }
     }
     ptx::cp_async_commit();
   };
 
-  int g = blockIdx.x;
-  if (g < ngroups) prefetch(g);
-  for (; g < ngroups; g += gridDim.x) {
-    ptx::cp_async_wait_all();
-    T x[CH];
+  // RP (register prefetch, LPT == 1): the next group's chunk is loaded straight
+  // into a second register set instead of the shared-memory landing zone
+  T nx[RP ? CH : 1];
+  auto prefetch_regs = [&](int g) {
+    const int off = line_off(g, 0);
+    const T* src = in + (off < 0 ? 0 : off);
 #pragma unroll
-    for (int k = 0; k < CH; ++k) x[k] = land[k * NT + tid];
-    if (g + int(gridDim.x) < ngroups) prefetch(g + gridDim.x);
-
-    // forward: local solve, exact carry scan over the chunks before this one
-    sf[w * 32 + lane] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
-    __syncthreads();
-    T c = T(0);
-    for (int v = 0; v < w; ++v) c = sf[v * 32 + lane] + tP[v * CH + CH - 1] * c;
-    ChunkSolve<T, CH>::apply(x, tP + s0, c);
-    // backward: local solve, carry scan over the chunks after this one
-    sb[w * 32 + lane] = ChunkSolve<T, CH>::bwd_local(x, tu + s0, tp + s0);
-    __syncthreads();
-    c = T(0);
-    for (int v = NC - 1; v > w; --v) c = sb[v * 32 + lane] + tQ[v * CH] * c;
-    ChunkSolve<T, CH>::apply(x, tQ + s0, c);
-
-    const int off = line_off(g);
-    if (off >= 0) {
-      T* dst = out + off;
+    for (int k = 0; k < CH; ++k) {
+      nx[k] = (off >= 0 && k < kmax) ? __ldg(src) : T(0);
+      if (k + 1 < kmax) src += sd;
+    }
+  };
+  int g = blockIdx.x;
+  if (g < ngroups) {
+    if constexpr (RP) prefetch_regs(g);
+    else prefetch(g);
+  }
+  for (; g < ngroups; g += gridDim.x) {
+    T x[LPT][CH];
+    if constexpr (RP) {
+#pragma unroll
+      for (int k = 0; k < CH; ++k) x[0][k] = nx[k];
+      if (g + int(gridDim.x) < ngroups) prefetch_regs(g + gridDim.x);
+    } else {
+      ptx::cp_async_wait_all();
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
-        if (k < kmax) *dst = x[k];
+        if constexpr (LPT == 2) {
+          using T2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+          const T2 v = *reinterpret_cast<const T2*>(land + (k * NT + tid) * 2);
+          x[0][k] = v.x;
+          x[1][k] = v.y;
+        } else {
+          x[0][k] = land[k * NT + tid];
+        }
+      }
+      if (g + int(gridDim.x) < ngroups) prefetch(g + gridDim.x);
+    }
+
+    // forward: local solve, exact carry scan over the chunks before this one
+    T e[LPT], c[LPT];
+    ChunkSolve<T, CH, LPT>::fwd_local(x, tm + s0, e);
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) sf[w * GW + LPT * lane + u] = e[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) c[u] = T(0);
+    for (int v = 0; v < w; ++v) {
+      const T pe = tP[v * CH + CH - 1];
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) c[u] = sf[v * GW + LPT * lane + u] + pe * c[u];
+    }
+    ChunkSolve<T, CH, LPT>::apply(x, tP + s0, c);
+    // backward: local solve, carry scan over the chunks after this one
+    ChunkSolve<T, CH, LPT>::bwd_local(x, tu + s0, tp + s0, e);
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) sb[w * GW + LPT * lane + u] = e[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) c[u] = T(0);
+    for (int v = NC - 1; v > w; --v) {
+      const T qs = tQ[v * CH];
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) c[u] = sb[v * GW + LPT * lane + u] + qs * c[u];
+    }
+    ChunkSolve<T, CH, LPT>::apply(x, tQ + s0, c);
+
+    if (g < nfull_groups) {
+      T* dst = out + line_off(g, 0);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        if (k < kmax) {
+#pragma unroll
+          for (int u = 0; u < LPT; ++u) dst[u] = x[u][k];
+        }
         dst += sd;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) {
+        const int off = line_off(g, u);
+        if (off < 0) continue;
+        T* dst = out + off;
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          if (k < kmax) *dst = x[u][k];
+          dst += sd;
+        }
       }
     }
   }
@@ -314,17 +431,22 @@ void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const
 template <class T, int CH>
 void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, const T* rpiv,
                const T* upper, cudaStream_t s) {
-  constexpr int NT = 32 * kLW, NP = kLW * CH;
-  const size_t smem = (size_t(5) * NP + 2 * kLW * 32 + size_t(CH) * NT) * sizeof(T);
-  auto kern = k_thomas_lines<T, CH>;
+  // fp32: the next group's chunk is prefetched into registers (fp64 chunks are
+  // too large for a second register set and go through the cp.async landing zone)
+  constexpr int LPT = 1;
+  constexpr bool RP = sizeof(T) == 4;
+  constexpr int NT = 32 * kLW, NP = kLW * CH, GW = 32 * LPT;
+  const size_t smem =
+      (size_t(5) * NP + 2 * kLW * GW + (RP ? 0 : size_t(CH) * NT * LPT)) * sizeof(T);
+  auto kern = k_thomas_lines<T, CH, LPT, RP>;
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int n = int(e[dim]);
   const int sd = int(dim == 0 ? e[1] * e[2] : e[2]);
   const int so = int(dim == 0 ? e[2] : e[1] * e[2]);  // stride of the other strided dim
   const int na = int(dim == 0 ? e[1] : e[0]);
   const int c2 = int(e[2]);
-  const int nfull = c2 / 32, ntail = c2 % 32;
-  const int groups = na * nfull + ((na + 31) / 32) * ntail;
+  const int nfull = c2 / GW, ntail = c2 % GW;
+  const int groups = na * nfull + ((na + GW - 1) / GW) * ntail;
   const int grid = groups < sm_count() ? groups : sm_count();
   kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, na, c2, nfull, ntail, groups, mult, rpiv, upper);
   HGR_CUDA_CHECK(cudaGetLastError());
