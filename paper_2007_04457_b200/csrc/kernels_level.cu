@@ -55,15 +55,15 @@ constexpr int kMaxSeg = 64;  // coarse planes per dim-0 segment (S0 <= kMaxSeg)
 
 template <class T>
 struct LCfg {
-  // fp64: lane = 1 coarse column, 2 column groups, 16 warps, one CTA per SM;
-  // fp32: lane = 2 coarse columns (16-byte loads), 1 group, 8 warps, two CTAs per SM
+  // fp64: lane = 1 coarse column, tile 16 x 32, 8 warps, two CTAs per SM;
+  // fp32: lane = 2 coarse columns (16-byte loads), tile 16 x 64, 8 warps, two CTAs per SM
   static constexpr int CPL = sizeof(T) == 8 ? 1 : 2;           // coarse columns per lane
-  static constexpr int NG = 2 / CPL;                           // column groups
-  static constexpr int NT = sizeof(T) == 8 ? 512 : 256, NW = NT / 32, WG = NW / NG;
-  static constexpr int MINB = sizeof(T) == 8 ? 1 : 2;          // CTAs per SM
-  static constexpr int TW2 = 64;                               // coarse columns
-  static constexpr int TW1 = sizeof(T) == 8 ? 14 : 16;         // coarse rows
-  static constexpr int NS = sizeof(T) == 8 ? 5 : 4;            // ring slots
+  static constexpr int NG = 1;                                 // column groups
+  static constexpr int NT = 256, NW = NT / 32, WG = NW / NG;
+  static constexpr int MINB = 2;                               // CTAs per SM
+  static constexpr int TW2 = 32 * CPL * NG;                    // coarse columns
+  static constexpr int TW1 = 16;                               // coarse rows
+  static constexpr int NS = 4;                                 // ring slots
   static constexpr int V = 16 / int(sizeof(T));                // elements per 16 bytes
   static constexpr int RW = 2 * TW1 + 3, CW = 2 * TW2 + 3;     // window rows / columns
   static constexpr int NB = TW1 / 2;                           // bands of 4 owned rows
