@@ -283,29 +283,25 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-// The last fine row (e1-1) and column (e2-1) of the level, every plane: one
-// thread per cell (reference-order multilinear interpolation, kernels.cuh).
+// The last fine column (e2-1, blockIdx.y = 0) and row (e1-1, columns < e2-1,
+// blockIdx.y = 1) of fine plane blockIdx.x: one thread per cell
+// (reference-order multilinear interpolation, kernels.cuh).
 template <class T>
 __global__ void __launch_bounds__(256)
     k_interp_face(const T* coef, T* out, const T* __restrict__ C, const T* __restrict__ Z,
                   LevelArgs<T> a, bool with) {
-  const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
-  const int64_t c1 = a.c[1], c2 = a.c[2];
-  const int64_t fA = e0 * e1, total = fA + e0 * (e2 - 1);
+  const int e1 = int(a.e[1]), e2 = int(a.e[2]);
+  const int c1 = int(a.c[1]), c2 = int(a.c[2]);
+  const int j = blockIdx.x, face = blockIdx.y;
   auto coarse = [&](int64_t q0, int64_t q1, int64_t q2) {
     const int64_t q = (q0 * c1 + q1) * c2 + q2;
     return Z ? C[q] - Z[q] : C[q];
   };
-  for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < total;
-       it += int64_t(gridDim.x) * blockDim.x) {
-    int64_t j, r, c;
-    if (it < fA) {
-      j = it / e1; r = it % e1; c = e2 - 1;
-    } else {
-      const int64_t q = it - fA;
-      j = q / (e2 - 1); r = e1 - 1; c = q % (e2 - 1);
-    }
-    const int64_t idx = (j * e1 + r) * e2 + c;
+  const int n = face == 0 ? e1 : e2 - 1;
+  const int64_t pbase = int64_t(j) * e1 * e2;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    const int r = face == 0 ? q : e1 - 1, c = face == 0 ? e2 - 1 : q;
+    const int64_t idx = pbase + int64_t(r) * e2 + c;
     if (((j | r | c) & 1) == 0) {
       out[idx] = coarse(j >> 1, r >> 1, c >> 1);
     } else {
@@ -375,8 +371,7 @@ bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const Leve
   else if (with) run_interp<T, true, false>(coef, out, C, Z, a, s);
   else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s);
   else run_interp<T, false, false>(coef, out, C, Z, a, s);
-  const int64_t face = a.e[0] * (a.e[1] + a.e[2] - 1);
-  k_interp_face<T><<<grid_for(face, 256), 256, 0, s>>>(coef, out, C, Z, a, with);
+  k_interp_face<T><<<dim3(unsigned(a.e[0]), 2), 256, 0, s>>>(coef, out, C, Z, a, with);
   HGR_CUDA_CHECK(cudaGetLastError());
   return true;
 }

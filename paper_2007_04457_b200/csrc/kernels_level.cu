@@ -490,72 +490,104 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   }
 }
 
-// Faces outside the tiles of k_level_fused: zload on the last coarse column
-// (c2-1, every coarse (i0, i1)) and the last coarse row (c1-1, i2 < c2-1) --
-// K0 (x) K1 (x) K2 applied directly, coarse nodes masked in recompose mode
-// (correction.hpp:251) -- plus, in decompose mode, the coefficients of the fine
-// cells on the last fine column / row (transforms.hpp:20-65), and in recompose
-// mode the gather of the coarse nodes on those faces. One thread per item.
+// Faces outside the tiles of k_level_fused. blockIdx.y selects the face:
+//   0: zload on the last coarse column (c2-1) of coarse plane i0 = blockIdx.x,
+//   1: zload on the last coarse row (c1-1, i2 < c2-1) of coarse plane i0,
+//   2: (decompose) coefficients of the fine cells on the last fine column of
+//      fine plane blockIdx.x, 3: ... on the last fine row (columns < e2-1).
+// Recompose mode masks the coarse nodes (correction.hpp:251) and gathers the
+// coarse nodes of faces 0/1. K0 (x) K1 (x) K2 is applied separably: the CTA
+// first reduces the 3 fine columns (rows) next to the face with K2 (K1) for the
+// 5 fine planes of its coarse plane into shared memory, then every thread forms
+// its output from 25 of those sums.
 template <class T, int MODE>
 __global__ void __launch_bounds__(256)
     k_level_face(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ zload,
                  T* __restrict__ gather, LevelArgs<T> a, int* flag) {
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
-  const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
-  const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
-  const int64_t nA = c0 * c1, nB = c0 * (c2 - 1);
-  const int64_t fA = DEC ? e0 * e1 : 0, fB = DEC ? e0 * (e2 - 1) : 0;
-  const int64_t total = nA + nB + fA + fB;
-  auto coarse = [&](int64_t b0, int64_t b1, int64_t b2) {
-    return U[((2 * b0) * e1 + 2 * b1) * e2 + 2 * b2];
-  };
-  for (int64_t it = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; it < total;
-       it += int64_t(gridDim.x) * blockDim.x) {
-    if (it < nA + nB) {
-      int64_t i0, i1, i2;
-      if (it < nA) {
-        i0 = it / c1; i1 = it % c1; i2 = c2 - 1;
-      } else {
-        const int64_t q = it - nA;
-        i0 = q / (c2 - 1); i1 = c1 - 1; i2 = q % (c2 - 1);
+  extern __shared__ __align__(16) unsigned char smem_f[];
+  T* Rs = reinterpret_cast<T*>(smem_f);  // [5][e] partial sums
+  const int e0 = int(a.e[0]), e1 = int(a.e[1]), e2 = int(a.e[2]);
+  const int c0 = int(a.c[0]), c1 = int(a.c[1]), c2 = int(a.c[2]);
+  const int face = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t plane = int64_t(e1) * e2;
+  if (face <= 1) {
+    const int i0 = blockIdx.x;
+    if (i0 >= c0) return;
+    const int ne = face == 0 ? e1 : e2;  // fine extent along the free dimension
+    // R[a][f] = sum over the 3 fine cells next to the face (K2 or K1 boundary row)
+    for (int idx = tid; idx < 5 * ne; idx += nt) {
+      const int x = idx / ne, f = idx - x * ne;
+      const int f0 = 2 * i0 - 2 + x;
+      T r = T(0);
+      if (f0 >= 0 && f0 < e0) {
+        for (int c = 0; c < 3; ++c) {
+          int f1, f2;
+          T w;
+          if (face == 0) {
+            f1 = f; f2 = e2 - 3 + c; w = a.taps[2][int64_t(c2 - 1) * 5 + c];
+          } else {
+            f1 = e1 - 3 + c; f2 = f; w = a.taps[1][int64_t(c1 - 1) * 5 + c];
+          }
+          const bool masked = REC && !((f0 | f1 | f2) & 1);
+          r += w * (masked ? T(0) : U[f0 * plane + int64_t(f1) * e2 + f2]);
+        }
       }
+      Rs[idx] = r;
+    }
+    __syncthreads();
+    const int nout = face == 0 ? c1 : c2 - 1;
+    for (int q = tid; q < nout; q += nt) {
       T acc = T(0);
       for (int x = 0; x < 5; ++x) {
-        const int64_t f0 = 2 * i0 - 2 + x;
+        const int f0 = 2 * i0 - 2 + x;
         if (f0 < 0 || f0 >= e0) continue;
-        const T w0 = e0 == 1 ? T(1) : a.taps[0][i0 * 5 + x];
+        const T w0 = e0 == 1 ? T(1) : a.taps[0][int64_t(i0) * 5 + x];
         T acc1 = T(0);
         for (int y = 0; y < 5; ++y) {
-          const int64_t f1 = 2 * i1 - 2 + y;
-          if (f1 < 0 || f1 >= e1) continue;
-          const T* row = U + (f0 * e1 + f1) * e2;
-          T acc2 = T(0);
-          for (int z = 0; z < 5; ++z) {
-            const int64_t f2 = 2 * i2 - 2 + z;
-            if (f2 < 0 || f2 >= e2) continue;
-            const bool masked = REC && !((f0 | f1 | f2) & 1);
-            acc2 += a.taps[2][i2 * 5 + z] * (masked ? T(0) : row[f2]);
-          }
-          acc1 += a.taps[1][i1 * 5 + y] * acc2;
+          const int f = 2 * q - 2 + y;
+          if (f < 0 || f >= ne) continue;
+          const T w = face == 0 ? a.taps[1][int64_t(q) * 5 + y] : a.taps[2][int64_t(q) * 5 + y];
+          acc1 += w * Rs[x * ne + f];
         }
         acc += w0 * acc1;
       }
-      const int64_t q = (i0 * c1 + i1) * c2 + i2;
-      zload[q] = acc;
-      if (REC) gather[q] = coarse(i0, i1, i2);
-    } else if (DEC) {
-      int64_t q = it - nA - nB, j, r, c;
-      if (q < fA) {
-        j = q / e1; r = q % e1; c = e2 - 1;
-      } else {
-        q -= fA;
-        j = q / (e2 - 1); r = e1 - 1; c = q % (e2 - 1);
-      }
-      const int64_t idx = (j * e1 + r) * e2 + c;
-      const T u = U[idx];
-      if (flag && !isfinite(u)) atomicOr(flag, 1);
-      if ((j | r | c) & 1) coef_out[idx] = u - interp_node(a, j, r, c, coarse);
+      const int i1 = face == 0 ? q : c1 - 1, i2 = face == 0 ? c2 - 1 : q;
+      const int64_t o = (int64_t(i0) * c1 + i1) * c2 + i2;
+      zload[o] = acc;
+      if (REC) gather[o] = U[(2 * int64_t(i0)) * plane + int64_t(2 * i1) * e2 + 2 * i2];
     }
+    return;
+  }
+  if (!DEC) return;
+  const int j = blockIdx.x;
+  if (j >= e0) return;
+  auto coarse = [&](int64_t b0, int64_t b1, int64_t b2) {
+    return U[(2 * b0) * plane + (2 * b1) * e2 + 2 * b2];
+  };
+  const int n = face == 2 ? e1 : e2 - 1;
+  bool bad = false;
+  for (int q = tid; q < n; q += nt) {
+    const int r = face == 2 ? q : e1 - 1, c = face == 2 ? e2 - 1 : q;
+    const int64_t idx = j * plane + int64_t(r) * e2 + c;
+    const T u = U[idx];
+    bad |= !isfinite(u);
+    if ((j | r | c) & 1) coef_out[idx] = u - interp_node(a, j, r, c, coarse);
+  }
+  if (flag && __syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
+}
+
+template <class T, int MODE>
+void set_level_face_smem(size_t bytes) {
+  static size_t set_bytes = 48 * 1024;
+  static int set_dev = -1;
+  int dev = 0;
+  HGR_CUDA_CHECK(cudaGetDevice(&dev));
+  if (bytes > 48 * 1024 && (bytes > set_bytes || dev != set_dev)) {
+    HGR_CUDA_CHECK(cudaFuncSetAttribute(k_level_face<T, MODE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    set_bytes = bytes;
+    set_dev = dev;
   }
 }
 
@@ -601,9 +633,10 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
     HGR_CUDA_CHECK(cudaGetLastError());
     sa = sb;
   }
-  const int64_t face_items = a.c[0] * (a.c[1] + a.c[2] - 1) +
-                             (MODE == kFusedDecompose ? a.e[0] * (a.e[1] + a.e[2] - 1) : 0);
-  k_level_face<T, MODE><<<grid_for(face_items, 256), 256, 0, s>>>(U, coef, z, gather, a, flag);
+  const dim3 fgrid(unsigned(std::max(a.c[0], a.e[0])), MODE == kFusedDecompose ? 4 : 2);
+  const size_t fsmem = size_t(5) * size_t(std::max(a.e[1], a.e[2])) * sizeof(T);
+  set_level_face_smem<T, MODE>(fsmem);
+  k_level_face<T, MODE><<<fgrid, 256, fsmem, s>>>(U, coef, z, gather, a, flag);
   HGR_CUDA_CHECK(cudaGetLastError());
 }
 
