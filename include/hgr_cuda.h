@@ -25,6 +25,7 @@
 #define HGR_CUDA_H
 
 #include <stddef.h>
+#include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -192,6 +193,38 @@ int hgr_cuda_masstrans_apply_f32(size_t n, size_t count, const float* d_v, const
                                  float* d_out, void* stream);
 int hgr_cuda_thomas_solve_f32(size_t n, size_t count, const float* d_rhs, const float* h_h,
                               float* d_out, void* stream);
+
+/* ---- the progressive .hg container (storage.hpp:17-218) ----------------------
+ * Files are byte-identical to hgr::write_file's. Classes are packed / unpacked
+ * on the device (extract_class / scatter_class order) and move as one
+ * contiguous payload through pinned staging buffers. Synchronous. */
+typedef struct hgr_hg_info {
+  unsigned version;          /* HgFileHeader (storage.hpp:36-55) */
+  unsigned precision_bytes;  /* 4 or 8 */
+  int rank;
+  size_t extents[3];
+  int class_count;
+  uint64_t header_bytes;
+  uint64_t file_bytes;
+} hgr_hg_info;
+/* read_info (storage.hpp:129-177): header and class table only */
+int hgr_hg_read_info(const char* path, hgr_hg_info* info);
+/* the coordinate table of dimension dim (extents[dim] values) */
+int hgr_hg_read_coords(const char* path, int dim, double* h_out);
+/* per-class (offset, byte length), coarse first; max_classes entries at most */
+int hgr_hg_read_class_table(const char* path, uint64_t* offsets, uint64_t* bytes, int max_classes);
+/* write_file (storage.hpp:86-126) of a device pyramid; *bytes_written = file size */
+int hgr_cuda_write_hg_f64(const char* path, const hgr_grid_desc* g, const double* d_pyramid,
+                          uint64_t* bytes_written, void* stream);
+int hgr_cuda_write_hg_f32(const char* path, const hgr_grid_desc* g, const float* d_pyramid,
+                          uint64_t* bytes_written, void* stream);
+/* read_prefix (storage.hpp:187-216): classes 0..upto_class into a zero-filled
+ * device pyramid of the file's extents (hgr_hg_read_info); *bytes_read = header
+ * plus the classes read */
+int hgr_cuda_read_hg_prefix_f64(const char* path, int upto_class, double* d_pyramid,
+                                uint64_t* bytes_read, void* stream);
+int hgr_cuda_read_hg_prefix_f32(const char* path, int upto_class, float* d_pyramid,
+                                uint64_t* bytes_read, void* stream);
 
 #ifdef __cplusplus
 }

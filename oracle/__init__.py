@@ -196,6 +196,26 @@ class Oracle:
         return data
 
     # -- reference-only helpers (seeded fixtures, worker count) ------------------
+    # storage.hpp (reference only): the .hg container
+    def write_file(self, pyramid, path, coords=None):
+        """hgr::write_file of a decomposed pyramid; returns the byte count."""
+        assert self.kind == "reference", "the .hg container exists in the reference only"
+        src = np.ascontiguousarray(pyramid)
+        g, _k = self._grid(src.shape, coords)
+        n = C.c_ulonglong(0)
+        self._check(self._fn("write_file_" + _dt(src))(C.byref(g), self._p(src),
+                                                       str(path).encode(), C.byref(n)))
+        return int(n.value)
+
+    def read_prefix(self, path, upto_class, shape, dtype):
+        """hgr::read_prefix: (zero-filled pyramid, bytes_read)."""
+        assert self.kind == "reference", "the .hg container exists in the reference only"
+        out = np.zeros(shape, dtype=dtype)
+        n = C.c_ulonglong(0)
+        self._check(self._fn("read_prefix_" + _dt(out))(str(path).encode(), int(upto_class),
+                                                        self._p(out), C.byref(n)))
+        return out, int(n.value)
+
     def set_worker_count(self, n: int) -> None:
         if self.kind != "reference":
             return

@@ -129,6 +129,24 @@ int scatter(const hgro_grid* g, T* data, int cls, const T* vals) {
   });
 }
 
+template <class T>
+int write_file_(const hgro_grid* g, const T* data, const char* path, unsigned long long* bytes) {
+  return guarded([&] {
+    auto grid = make_grid(g);
+    hgr::RefactoredArray<T> r{wrap(grid.finest_extents(), data), grid};
+    *bytes = hgr::write_file(r, path);
+  });
+}
+
+template <class T>
+int read_prefix_(const char* path, int upto, T* out, unsigned long long* bytes) {
+  return guarded([&] {
+    auto pr = hgr::read_prefix<T>(path, upto);
+    std::memcpy(out, pr.array.data.data(), pr.array.data.size() * sizeof(T));
+    *bytes = pr.bytes_read;
+  });
+}
+
 }  // namespace
 
 extern "C" {
@@ -175,6 +193,13 @@ std::size_t hgrref_worker_count(void) { return hgr::worker_count(); }
   }                                                                                            \
   int hgrref_scatter_class_##S(const hgro_grid* g, T* d, int c, const T* v) {                  \
     return scatter<T>(g, d, c, v);                                                             \
+  }                                                                                            \
+  int hgrref_write_file_##S(const hgro_grid* g, const T* d, const char* p,                     \
+                            unsigned long long* b) {                                           \
+    return write_file_<T>(g, d, p, b);                                                         \
+  }                                                                                            \
+  int hgrref_read_prefix_##S(const char* p, int m, T* o, unsigned long long* b) {             \
+    return read_prefix_<T>(p, m, o, b);                                                        \
   }
 
 REF_EXPORTS(double, f64)

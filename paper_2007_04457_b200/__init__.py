@@ -457,3 +457,88 @@ def masstrans_apply(v, h):
 def thomas_solve(rhs, h):
     """thomas_solve (correction.hpp:217-223)."""
     return _fiber("thomas_solve", rhs, h, lambda n: n)
+
+
+# ---- the progressive .hg container (storage.hpp:17-218) ------------------------
+
+@dataclass
+class HgFileHeader:
+    """storage.hpp:36-55."""
+    version: int
+    precision_bytes: int
+    rank: int
+    extents: list
+    coords: list
+    class_offsets: list
+    class_bytes: list
+    header_bytes: int
+    file_bytes: int
+
+    def class_count(self) -> int:
+        return len(self.class_bytes)
+
+    def class_elements(self, cls: int) -> int:
+        return self.class_bytes[cls] // self.precision_bytes
+
+    def total_elements(self) -> int:
+        n = 1
+        for e in self.extents:
+            n *= e
+        return n
+
+
+def write_file(r: RefactoredArray, path) -> int:
+    """hgr::write_file (storage.hpp:86-126) of a pyramid held on the device (or
+    host: it is staged to the current device). Classes are packed on the GPU;
+    the file is byte-identical to the reference's. Returns the byte count."""
+    import torch
+    lib = _lib.load()
+    data = r.data if _is_torch(r.data) else torch.from_numpy(np.ascontiguousarray(r.data)).cuda()
+    data = data.contiguous()
+    _check_shape(data, r.hierarchy, "write_file")
+    n = C.c_uint64(0)
+    _check(getattr(lib, f"hgr_cuda_write_hg_{_dtype_tag(data)}")(
+        str(path).encode(), C.byref(r.hierarchy.desc), _ptr(data), C.byref(n), _stream_of(data)))
+    return int(n.value)
+
+
+def read_info(path) -> HgFileHeader:
+    """hgr::read_info (storage.hpp:129-177): header and class table only."""
+    lib = _lib.load()
+    info = _lib.HgInfo()
+    p = str(path).encode()
+    _check(lib.hgr_hg_read_info(p, C.byref(info)))
+    rank = info.rank
+    extents = [int(info.extents[d]) for d in range(rank)]
+    coords = []
+    for d in range(rank):
+        c = np.empty(extents[d], np.float64)
+        _check(lib.hgr_hg_read_coords(p, d, c.ctypes.data))
+        coords.append(c)
+    nc = info.class_count
+    offs, byts = np.zeros(nc, np.uint64), np.zeros(nc, np.uint64)
+    _check(lib.hgr_hg_read_class_table(p, offs.ctypes.data, byts.ctypes.data, nc))
+    return HgFileHeader(int(info.version), int(info.precision_bytes), rank, extents, coords,
+                        [int(v) for v in offs], [int(v) for v in byts], int(info.header_bytes),
+                        int(info.file_bytes))
+
+
+@dataclass
+class PrefixRead:
+    array: RefactoredArray
+    bytes_read: int
+
+
+def read_prefix(path, upto_class: int, dtype: Optional[str] = None, device=None) -> PrefixRead:
+    """hgr::read_prefix (storage.hpp:187-216): classes 0..upto_class into a
+    zero-filled device pyramid (classes are scattered on the GPU)."""
+    import torch
+    h = read_info(path)
+    dt = dtype or ("f64" if h.precision_bytes == 8 else "f32")
+    g = GridHierarchy(h.coords)
+    out = torch.empty(h.extents, dtype=torch.float64 if dt == "f64" else torch.float32,
+                      device=device or "cuda")
+    n = C.c_uint64(0)
+    _check(getattr(_lib.load(), f"hgr_cuda_read_hg_prefix_{dt}")(
+        str(path).encode(), int(upto_class), _ptr(out), C.byref(n), _stream_of(out)))
+    return PrefixRead(RefactoredArray(out, g), int(n.value))

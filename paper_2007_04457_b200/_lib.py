@@ -19,6 +19,13 @@ class GridDesc(C.Structure):
     _fields_ = [("rank", C.c_int), ("extents", C.c_size_t * 3), ("coords", C.c_void_p * 3)]
 
 
+class HgInfo(C.Structure):
+    """hgr_hg_info = HgFileHeader (storage.hpp:36-55)."""
+    _fields_ = [("version", C.c_uint), ("precision_bytes", C.c_uint), ("rank", C.c_int),
+                ("extents", C.c_size_t * 3), ("class_count", C.c_int),
+                ("header_bytes", C.c_uint64), ("file_bytes", C.c_uint64)]
+
+
 _vp, _sz, _int = C.c_void_p, C.c_size_t, C.c_int
 _G = C.POINTER(GridDesc)
 
@@ -40,6 +47,9 @@ _SIGS = {
     "hgr_cuda_synthetic_field_f32": (_int, [_G, _vp, C.c_ulonglong, _vp, _vp, _vp, _vp]),
     "hgr_class_node_count": (_sz, [_G, _int]),
     "hgr_levels": (_int, [_G]),
+    "hgr_hg_read_info": (_int, [C.c_char_p, C.POINTER(HgInfo)]),
+    "hgr_hg_read_coords": (_int, [C.c_char_p, _int, _vp]),
+    "hgr_hg_read_class_table": (_int, [C.c_char_p, _vp, _vp, _int]),
 }
 for _t in ("f64", "f32"):
     _SIGS.update({
@@ -55,6 +65,9 @@ for _t in ("f64", "f32"):
         f"hgr_cuda_scatter_class_{_t}": (_int, [_G, _vp, _int, _vp, _vp]),
         f"hgr_cuda_masstrans_apply_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
         f"hgr_cuda_thomas_solve_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
+        f"hgr_cuda_write_hg_{_t}": (_int, [C.c_char_p, _G, _vp, C.POINTER(C.c_uint64), _vp]),
+        f"hgr_cuda_read_hg_prefix_{_t}": (_int, [C.c_char_p, _int, _vp, C.POINTER(C.c_uint64),
+                                                   _vp]),
     })
 _SIGS["hgr_cuda_mass_apply_f64"] = (_int, [_sz, _sz, _vp, _vp, _vp, _vp])
 

@@ -10,6 +10,7 @@
 #include "../../include/hgr_cuda.h"
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "storage.hpp"
 
 using hgrb::Error;
 using hgrb::Plan;
@@ -483,6 +484,92 @@ int hgr_cuda_masstrans_apply_f32(size_t n, size_t c, const float* v, const float
 }
 int hgr_cuda_thomas_solve_f32(size_t n, size_t c, const float* v, const float* h, float* o, void* s) {
   return fiber_op(2, n, c, v, h, o, s);
+}
+
+}  // extern "C"
+
+// ---- .hg container (storage.hpp:17-218) ---------------------------------------
+
+namespace {
+
+template <class T>
+int write_hg(const char* path, const hgr_grid_desc* g, const T* d, uint64_t* bytes, void* s) {
+  return guarded([&] {
+    hgrb::require(path != nullptr, "path is null");
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    const uint64_t n = hgrb::hg_write(path, *p, d, as_stream(s));
+    if (bytes) *bytes = n;
+  });
+}
+
+template <class T>
+int read_hg_prefix(const char* path, int upto, T* d, uint64_t* bytes, void* s) {
+  return guarded([&] {
+    hgrb::require(path != nullptr, "path is null");
+    const hgrb::HgInfo info = hgrb::hg_read_info(path);
+    hgr_grid_desc g{};
+    g.rank = info.rank;
+    for (int k = 0; k < info.rank; ++k) {
+      g.extents[k] = info.extents[std::size_t(k)];
+      g.coords[k] = info.coords[std::size_t(k)].data();
+    }
+    auto p = cached_plan(&g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    const uint64_t n = hgrb::hg_read_prefix(path, info, *p, upto, d, as_stream(s));
+    if (bytes) *bytes = n;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int hgr_hg_read_info(const char* path, hgr_hg_info* out) {
+  return guarded([&] {
+    hgrb::require(path != nullptr && out != nullptr, "null argument");
+    const hgrb::HgInfo h = hgrb::hg_read_info(path);
+    *out = hgr_hg_info{};
+    out->version = h.version;
+    out->precision_bytes = h.precision_bytes;
+    out->rank = h.rank;
+    for (int k = 0; k < h.rank; ++k) out->extents[k] = h.extents[std::size_t(k)];
+    out->class_count = int(h.offsets.size());
+    out->header_bytes = h.header_bytes;
+    out->file_bytes = h.file_bytes;
+  });
+}
+
+int hgr_hg_read_coords(const char* path, int dim, double* h_out) {
+  return guarded([&] {
+    const hgrb::HgInfo h = hgrb::hg_read_info(path);
+    hgrb::require(dim >= 0 && dim < h.rank, "dimension out of range");
+    const auto& c = h.coords[std::size_t(dim)];
+    std::memcpy(h_out, c.data(), c.size() * sizeof(double));
+  });
+}
+
+int hgr_hg_read_class_table(const char* path, uint64_t* offsets, uint64_t* bytes, int max_classes) {
+  return guarded([&] {
+    const hgrb::HgInfo h = hgrb::hg_read_info(path);
+    for (std::size_t c = 0; c < h.offsets.size() && int(c) < max_classes; ++c) {
+      if (offsets) offsets[c] = h.offsets[c];
+      if (bytes) bytes[c] = h.bytes[c];
+    }
+  });
+}
+
+int hgr_cuda_write_hg_f64(const char* path, const hgr_grid_desc* g, const double* d, uint64_t* b,
+                          void* s) {
+  return write_hg(path, g, d, b, s);
+}
+int hgr_cuda_write_hg_f32(const char* path, const hgr_grid_desc* g, const float* d, uint64_t* b,
+                          void* s) {
+  return write_hg(path, g, d, b, s);
+}
+int hgr_cuda_read_hg_prefix_f64(const char* path, int upto, double* d, uint64_t* b, void* s) {
+  return read_hg_prefix(path, upto, d, b, s);
+}
+int hgr_cuda_read_hg_prefix_f32(const char* path, int upto, float* d, uint64_t* b, void* s) {
+  return read_hg_prefix(path, upto, d, b, s);
 }
 
 }  // extern "C"
