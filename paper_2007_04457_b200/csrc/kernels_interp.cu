@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* barf = reinterpret_cast<uint64_t*>(smem + C::bar_off);
   uint64_t* barc = barf + NS;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = ptx::warp_id_uniform();
   const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
   const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
   int bid = blockIdx.x;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(512, 1)
   auto issue_f = [&](int64_t j) {  // fine plane j into slot (j - jlo) % NS
     const int sl = int(j - jlo) % NS;
     if (tid == 0) ptx::mbar_arrive_expect_tx(&barf[sl], tx_f);
-    if (lane == 0) {
+    if (ptx::elect_one()) {
       T* dst = ring + sl * SLOT;
       const int64_t base = (j * e1 + 2 * q1a) * e2 + 2 * q2a - coef_off;
       for (int r = warp; r < frows; r += NW) {
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(512, 1)
   auto issue_c = [&](int64_t m) {  // coarse plane m into buffer m & 1
     const int bsl = int(m & 1);
     if (tid == 0) ptx::mbar_arrive_expect_tx(&barc[bsl], tx_c);
-    if (lane == 0) {
+    if (ptx::elect_one()) {
       T* dst = cbuf + bsl * 2 * CSLOT;
       const int64_t base = (m * c1 + q1a) * c2 + q2a - c_off;
       for (int r = warp; r < crows; r += NW) {

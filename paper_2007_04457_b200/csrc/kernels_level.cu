@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   T* w0t = reinterpret_cast<T*>(smem + C::w0_off);  // [2][W0N]: wl, wr of dim-0 intervals
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::bar_off);
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = ptx::warp_id_uniform();
   const int64_t e0 = a.e[0], e1 = a.e[1], e2 = a.e[2];
   const int64_t c0 = a.c[0], c1 = a.c[1], c2 = a.c[2];
   const int64_t plane_sz = e1 * e2;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   auto issue = [&](int64_t jj) {
     const int sl = int(jj - j0) % NS;
     if (tid == 0) ptx::mbar_arrive_expect_tx(&bar[sl], tx_bytes);
-    if (lane == 0) {
+    if (ptx::elect_one()) {
       T* dst = raw + sl * SLOT + warp * PITCH;
       const uint32_t pb = uint32_t(uint64_t(jj * plane_sz));
 #pragma unroll

@@ -9,6 +9,20 @@
 namespace hgrb {
 namespace ptx {
 
+// one elected lane of the (converged) warp, as a predicate
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+// warp index broadcast from lane 0, so the compiler can treat it as warp-uniform
+__device__ __forceinline__ int warp_id_uniform() {
+  return __shfl_sync(0xffffffffu, int(threadIdx.x) >> 5, 0);
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
