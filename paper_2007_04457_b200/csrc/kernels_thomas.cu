@@ -128,6 +128,16 @@ struct ChunkSolve {
   }
 };
 
+// Carry-scan depth: every forward multiplier m_i = h_i / p_i and backward
+// factor u_i / p_i is at most 1/2 (p_i >= 2 h_i + 1.5 h_{i-1}, the first is 1/2),
+// so a chunk of CH positions scales the carry through it by at most 2^-CH.
+// Chunks further than KD chunks away contribute below 2^-B (B = 56 for fp64, 26
+// for fp32) of their summaries and the scan stops there.
+template <class T, int CH>
+constexpr int scan_depth() {
+  return ((sizeof(T) == 8 ? 56 : 26) + CH - 1) / CH + 1;
+}
+
 // ---- strided lines (dims 0 / 1) ---------------------------------------------------
 
 constexpr int kLW = 16;  // warps (= chunks per line) of k_thomas_lines
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < LPT; ++u) c[u] = T(0);
-    for (int v = 0; v < w; ++v) {
+    for (int v = w > scan_depth<T, CH>() ? w - scan_depth<T, CH>() : 0; v < w; ++v) {
       const T pe = tP[v * CH + CH - 1];
 #pragma unroll
       for (int u = 0; u < LPT; ++u) c[u] = sf[v * GW + LPT * lane + u] + pe * c[u];
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < LPT; ++u) c[u] = T(0);
-    for (int v = NC - 1; v > w; --v) {
+    for (int v = w + scan_depth<T, CH>() < NC - 1 ? w + scan_depth<T, CH>() : NC - 1; v > w; --v) {
       const T qs = tQ[v * CH];
 #pragma unroll
       for (int u = 0; u < LPT; ++u) c[u] = sb[v * GW + LPT * lane + u] + qs * c[u];
@@ -366,12 +376,14 @@ __global__ void __launch_bounds__(512, 1)
     sf[q * R + r] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
     __syncthreads();
     T c = T(0);
-    for (int v = 0; v < q; ++v) c = sf[v * R + r] + tP[v * CH + CH - 1] * c;
+    for (int v = q > scan_depth<T, CH>() ? q - scan_depth<T, CH>() : 0; v < q; ++v)
+      c = sf[v * R + r] + tP[v * CH + CH - 1] * c;
     ChunkSolve<T, CH>::apply(x, tP + s0, c);
     sb[q * R + r] = ChunkSolve<T, CH>::bwd_local(x, tu + s0, tp + s0);
     __syncthreads();
     c = T(0);
-    for (int v = NC - 1; v > q; --v) c = sb[v * R + r] + tQ[v * CH] * c;
+    for (int v = q + scan_depth<T, CH>() < NC - 1 ? q + scan_depth<T, CH>() : NC - 1; v > q; --v)
+      c = sb[v * R + r] + tQ[v * CH] * c;
     ChunkSolve<T, CH>::apply(x, tQ + s0, c);
 
 #pragma unroll
