@@ -31,16 +31,24 @@ constexpr int kMaxSegI = 32;  // coarse planes per dim-0 segment
 
 template <class T>
 struct ICfg {
-  static constexpr int NT = 512, NW = 16, NG = 2, WG = NW / NG;
-  static constexpr int TW2 = 64, TW1 = sizeof(T) == 8 ? 14 : 16;
-  static constexpr int NS = sizeof(T) == 8 ? 5 : 7;            // coefficient plane slots
+  // fp64: lane = 1 coarse column, 16 warps in 2 column groups, one CTA per SM;
+  // fp32: lane = 2 coarse columns (float4 coefficient loads), 8 warps, two CTAs per SM
+  static constexpr bool D = sizeof(T) == 8;
+  static constexpr int CPL = D ? 1 : 2;
+  static constexpr int NG = D ? 2 : 1;
+  static constexpr int NT = D ? 512 : 256, NW = NT / 32, WG = NW / NG;
+  static constexpr int MINB = D ? 1 : 2;
+  static constexpr int TW2 = 32 * CPL * NG, TW1 = D ? 14 : 16;
+  static constexpr int NS = D ? 5 : 4;                         // coefficient plane slots
   static constexpr int V = 16 / int(sizeof(T));
   static constexpr int ALN = 128 / int(sizeof(T));
   static constexpr int FR = 2 * TW1, FC = 2 * TW2;             // fine rows / cols of a tile
   static constexpr int NB = FR / 4;                            // bands of four fine rows
   static_assert(NB <= WG, "one band per warp of a group");
+  static constexpr int NCELL = 2 * CPL;
   static constexpr int BOX = (FC + V - 1 + V - 1) / V * V;     // aligned superset of a row
   static constexpr int PITCH = (BOX + ALN - 1) / ALN * ALN;
+  static_assert(PITCH >= FC + V + 4, "vector reads stay inside the row");
   static constexpr int SLOT = FR * PITCH;
   static constexpr int CR = TW1 + 1, CC = TW2 + 1;             // coarse window
   static constexpr int CBOX = (CC + V - 1 + V - 1) / V * V;
@@ -51,7 +59,7 @@ struct ICfg {
   static constexpr int W0N = kMaxSegI + 2;
   static constexpr size_t bar_off = (w_off + size_t(2) * W0N * sizeof(T) + 15) / 16 * 16;
   static constexpr size_t total = bar_off + (NS + 2) * sizeof(uint64_t);
-  static_assert(total <= 227 * 1024, "shared memory budget");
+  static_assert(total * MINB <= 227 * 1024, "shared memory budget");
 };
 
 template <class T>
@@ -61,22 +69,40 @@ struct Vec2i<double> { using type = double2; };
 template <>
 struct Vec2i<float> { using type = float2; };
 
-// v[k] = row[pos + k], k < 2
-template <class T>
-__device__ __forceinline__ void ld2(const T* row, int pos, T& v0, T& v1) {
+// v[k] = row[pos + k], k < N (pairs by 2-element vector loads; fp32 N = 4 by float4)
+template <class T, int N>
+__device__ __forceinline__ void ldn(const T* row, int pos, T (&v)[N]) {
   using T2 = typename Vec2i<T>::type;
-  if (!(pos & 1)) {
-    const T2 x = *reinterpret_cast<const T2*>(row + pos);
-    v0 = x.x;
-    v1 = x.y;
+  if constexpr (N == 4 && sizeof(T) == 4) {
+    const int base = pos & ~3, ph = pos & 3;
+    const float4* p = reinterpret_cast<const float4*>(row + base);
+    const float4 x = p[0];
+    if (ph == 0) {
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+      const float4 y = p[1];
+      const float w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+      if (ph == 1) { v[0] = w[1]; v[1] = w[2]; v[2] = w[3]; v[3] = w[4]; }
+      else if (ph == 2) { v[0] = w[2]; v[1] = w[3]; v[2] = w[4]; v[3] = w[5]; }
+      else { v[0] = w[3]; v[1] = w[4]; v[2] = w[5]; v[3] = w[6]; }
+    }
+  } else if constexpr (N == 2) {
+    if (!(pos & 1)) {
+      const T2 x = *reinterpret_cast<const T2*>(row + pos);
+      v[0] = x.x;
+      v[1] = x.y;
+    } else {
+      v[0] = row[pos];
+      v[1] = row[pos + 1];
+    }
   } else {
-    v0 = row[pos];
-    v1 = row[pos + 1];
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = row[pos + k];
   }
 }
 
 template <class T, bool WITH, bool HASZ>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     k_interp_march(const __grid_constant__ CUtensorMap mcoef, const __grid_constant__ CUtensorMap mC,
                    const __grid_constant__ CUtensorMap mZ, int64_t coef_off, int64_t c_off,
                    T* __restrict__ out, LevelArgs<T> a, int S0, int nt1, int nt2, int nseg,
@@ -84,7 +110,7 @@ __global__ void __launch_bounds__(512, 1)
   using C = ICfg<T>;
   constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NW = C::NW;
   constexpr int TW1 = C::TW1, TW2 = C::TW2, WG = C::WG, NB = C::NB;
-  constexpr int CPITCH = C::CPITCH, CSLOT = C::CSLOT;
+  constexpr int CPITCH = C::CPITCH, CSLOT = C::CSLOT, CPL = C::CPL, NCELL = C::NCELL;
   extern __shared__ __align__(128) unsigned char smem[];
   T* ring = reinterpret_cast<T*>(smem);
   T* cbuf = reinterpret_cast<T*>(smem + C::c_off);
@@ -110,19 +136,20 @@ __global__ void __launch_bounds__(512, 1)
   const int frows = 2 * tw1;
 
   const int grp = warp / WG, wg = warp % WG;
-  const int t = 32 * grp + lane;  // tile-local coarse column
-  const int64_t tg = q2a + t;
-  const bool tvalid = t < tw2;
-  T hl = T(0), hr = T(0);
-  if (tvalid) {
-    hl = a.wl[2][tg];
-    hr = a.wr[2][tg];
+  const int t0 = CPL * (32 * grp + lane);  // tile-local coarse columns t0..t0+CPL-1
+  T hl[CPL], hr[CPL];
+  bool cvalid[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    cvalid[c] = t0 + c < tw2;
+    hl[c] = cvalid[c] ? a.wl[2][q2a + t0 + c] : T(0);
+    hr[c] = cvalid[c] ? a.wr[2][q2a + t0 + c] : T(0);
   }
   const bool has_band = wg < NB;
   const int b = 4 * wg;  // fine rows b..b+3 of the tile; coarse rows b/2 .. b/2+2
   bool rown[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) rown[i] = has_band && tvalid && b + i < frows;
+  for (int i = 0; i < 4; ++i) rown[i] = has_band && b + i < frows;
   T w1l[2] = {T(0), T(0)}, w1r[2] = {T(0), T(0)};  // odd fine rows b+1, b+3
   if (has_band) {
 #pragma unroll
@@ -184,16 +211,18 @@ __global__ void __launch_bounds__(512, 1)
   const int fph0 = int((2 * q1a * e2 + 2 * q2a) & (V - 1));
   const int cph0 = int((q1a * c2 + q2a) & (V - 1));
   auto fpos = [&](int64_t j, int r) {
-    return int((j * plane_f + fph0 + int64_t(r) * e2m) & (V - 1)) + 2 * t;
+    return int((j * plane_f + fph0 + int64_t(r) * e2m) & (V - 1)) + 2 * t0;
   };
   auto cpos = [&](int64_t m, int s) {
-    return int((m * plane_c + cph0 + int64_t(s) * c2m) & (V - 1)) + t;
+    return int((m * plane_c + cph0 + int64_t(s) * c2m) & (V - 1)) + t0;
   };
 
-  T A1p[4][2], A1[4][2];
+  T A1p[4][NCELL], A1[4][NCELL];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) A1p[i][0] = A1p[i][1] = A1[i][0] = A1[i][1] = T(0);
-  T* obase = out + (2 * q1a + b) * e2 + 2 * q2a + 2 * t;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[i][k] = T(0);
+  T* obase = out + (2 * q1a + b) * e2 + 2 * q2a + 2 * t0;
 
   // one fine plane j: out = coef + interp (interp alone at coarse nodes / without coef)
   auto fine_plane = [&](int64_t j, bool odd, T w0l, T w0r) {
@@ -204,25 +233,21 @@ __global__ void __launch_bounds__(512, 1)
     T* o = obase + j * plane_f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      T ip0, ip1;
-      if (odd) {
-        ip0 = w0l * A1p[i][0] + w0r * A1[i][0];
-        ip1 = w0l * A1p[i][1] + w0r * A1[i][1];
-      } else {
-        ip0 = A1[i][0];
-        ip1 = A1[i][1];
-      }
-      T v0 = ip0, v1 = ip1;
+      T v[NCELL];
+#pragma unroll
+      for (int k = 0; k < NCELL; ++k) v[k] = odd ? w0l * A1p[i][k] + w0r * A1[i][k] : A1[i][k];
       if (WITH) {
-        T c0v, c1v;
-        ld2<T>(S + (b + i) * PITCH, fpos(j, b + i), c0v, c1v);
-        // the coarse node (even plane, even row, even column) keeps the interpolant
-        if (odd || (i & 1)) v0 += c0v;
-        v1 += c1v;
+        T cf[NCELL];
+        ldn<T, NCELL>(S + (b + i) * PITCH, fpos(j, b + i), cf);
+#pragma unroll
+        for (int k = 0; k < NCELL; ++k)
+          // the coarse nodes (even plane, even row, even column) keep the interpolant
+          if (odd || (i & 1) || (k & 1)) v[k] += cf[k];
       }
       if (rown[i]) {
-        o[int64_t(i) * e2] = v0;
-        o[int64_t(i) * e2 + 1] = v1;
+#pragma unroll
+        for (int k = 0; k < NCELL; ++k)
+          if (cvalid[k >> 1]) o[int64_t(i) * e2 + k] = v[k];
       }
     }
   };
@@ -233,30 +258,27 @@ __global__ void __launch_bounds__(512, 1)
     ptx::mbar_wait(&barc[bsl], uint32_t(((m - ka) >> 1) & 1));
     if (has_band) {
       const T* Cb = cbuf + bsl * 2 * CSLOT;
-      T Cc[3][2];
+      T A2[3][NCELL];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const int s = b / 2 + k;
         const int ps = cpos(m, s);
-        T x0, x1;
-        ld2<T>(Cb + s * CPITCH, ps, x0, x1);
+        T x[CPL + 1];
+        ldn<T, CPL + 1>(Cb + s * CPITCH, ps, x);
         if (HASZ) {
-          T z0, z1;
-          ld2<T>(Cb + CSLOT + s * CPITCH, ps, z0, z1);
-          x0 -= z0;
-          x1 -= z1;
+          T z[CPL + 1];
+          ldn<T, CPL + 1>(Cb + CSLOT + s * CPITCH, ps, z);
+#pragma unroll
+          for (int c = 0; c <= CPL; ++c) x[c] -= z[c];
         }
-        Cc[k][0] = x0;
-        Cc[k][1] = x1;
-      }
-      T A2[3][2];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        A2[k][0] = Cc[k][0];
-        A2[k][1] = hl * Cc[k][0] + hr * Cc[k][1];
+        for (int c = 0; c < CPL; ++c) {
+          A2[k][2 * c] = x[c];
+          A2[k][2 * c + 1] = hl[c] * x[c] + hr[c] * x[c + 1];
+        }
       }
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < NCELL; ++c) {
         A1[0][c] = A2[0][c];
         A1[1][c] = w1l[0] * A2[0][c] + w1r[0] * A2[1][c];
         A1[2][c] = A2[1][c];
@@ -270,10 +292,9 @@ __global__ void __launch_bounds__(512, 1)
     }
     if (2 * m <= jhi) fine_plane(2 * m, false, T(0), T(0));
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      A1p[i][0] = A1[i][0];
-      A1p[i][1] = A1[i][1];
-    }
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[i][k];
     __syncthreads();  // slots of planes 2m-1, 2m and coarse buffer m are free
     if (WITH) {
       if (m > ka && 2 * m - 1 + NS <= jhi) issue_f(2 * m - 1 + NS);
