@@ -205,6 +205,23 @@ std::size_t hgrref_worker_count(void) { return hgr::worker_count(); }
 REF_EXPORTS(double, f64)
 REF_EXPORTS(float, f32)
 
+// perf_model.hpp:71-98 (the CLI's rank-configs)
+double hgrref_estimate_time(int kind, unsigned long long bx, unsigned long long by,
+                            unsigned long long bz, unsigned long long n, unsigned long long S,
+                            unsigned long long L, unsigned long long G, double bw) {
+  hgr::PerfParams p;
+  p.n = n;
+  p.transaction_bytes = S;
+  p.element_bytes = L;
+  p.ghost_elements = G;
+  p.peak_bandwidth = bw;
+  const hgr::KernelKind k = kind == 0 ? hgr::KernelKind::gpk
+                            : kind == 1 ? hgr::KernelKind::lpk : hgr::KernelKind::ipk;
+  double t = -1;
+  guarded([&] { t = hgr::estimate_time(k, hgr::KernelConfig{bx, by, bz}, p); });
+  return t;
+}
+
 // Seeded fixtures exactly as the reference's tests draw them
 // (tests/oracle_helpers.hpp:230-246): libstdc++ mt19937 + uniform_real.
 void hgrref_random_coords(std::size_t n, unsigned seed, double* out) {

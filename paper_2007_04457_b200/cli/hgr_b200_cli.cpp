@@ -10,8 +10,14 @@
 //   hgr-b200 recompose --input HG --classes K --output RAW [--json]
 //   hgr-b200 info --input HG [--json]
 //   hgr-b200 error --original RAW --reconstruction RAW [--precision f32|f64] [--json]
+//   hgr-b200 rank-configs [--n N] [--bytes-per-element B] [--transaction-bytes S]
+//                         [--ghost G] [--peak-bw BW] [--kernel gpk|lpk|ipk|all]
+//                         [--configs FILE] [--top K] [--json]
+//     (the paper's analytical launch-configuration cost model, perf_model.hpp:71-162;
+//      host arithmetic, kept so the reference's CLI surface is complete)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
@@ -349,9 +355,132 @@ int run_error(const std::string& original, const std::string& recon, bool as_jso
   return 0;
 }
 
+
+// ---- rank-configs (hgr_main.cpp:230-286; perf_model.hpp:71-162) ------------------
+struct KCfg {
+  uint64_t bx = 1, by = 1, bz = 1;
+};
+
+double estimate_time(int kind, const KCfg& c, uint64_t n, uint64_t S, uint64_t L, uint64_t G,
+                     double bw) {
+  require(c.bx >= 1 && c.by >= 1 && c.bz >= 1, "thread-block dimensions must be positive");
+  require(n >= 1, "problem size must be positive");
+  require(S >= 1 && L >= 1, "byte sizes must be positive");
+  require(S % L == 0, "transaction size must be a multiple of the element size");
+  require(bw > 0, "peak bandwidth must be positive");
+  auto cdiv = [](uint64_t a, uint64_t b) { return (a + b - 1) / b; };
+  auto pad = [&](uint64_t e, uint64_t per) { return cdiv(e, per) * per; };
+  const uint64_t spl = S / L, ghost = G ? G : spl;
+  const uint64_t bxn = cdiv(n, c.bx), byn = cdiv(n, c.by), bzn = cdiv(n, c.bz);
+  uint64_t touched = 0;
+  if (kind == 0)
+    touched = pad(c.bx + 1, spl) * (c.by + 1) * (c.bz + 1) * bxn * byn * bzn;
+  else if (kind == 1)
+    touched = (pad(c.bx, spl) + 2 * spl) * c.by * c.bz * bxn * byn * bzn;
+  else
+    touched = (pad(ghost, spl) + pad(c.bx, spl) * bxn) * c.by * c.bz * byn * bzn;
+  return double(touched) * 2.0 * double(L) / bw;
+}
+
+int run_rank_configs(const Args& a, int& stage) {
+  auto u64 = [&](const std::string& k, uint64_t d) {
+    const std::string v = one(a, k, "", false);
+    if (v.empty()) return d;
+    try {
+      std::size_t pos = 0;
+      const unsigned long long x = std::stoull(v, &pos);
+      if (pos != v.size()) throw std::invalid_argument(v);
+      return uint64_t(x);
+    } catch (const std::exception&) {
+      throw UsageError(k + ": not a non-negative integer");
+    }
+  };
+  const uint64_t n = u64("--n", 513), L = u64("--bytes-per-element", 8);
+  const uint64_t S = u64("--transaction-bytes", 32), G = u64("--ghost", 0);
+  const uint64_t top = u64("--top", 0);
+  double bw = 1.0;
+  if (a.opt.count("--peak-bw")) {
+    try {
+      bw = std::stod(one(a, "--peak-bw"));
+    } catch (const std::exception&) {
+      throw UsageError("--peak-bw: not a number");
+    }
+  }
+  const std::string kernel = one(a, "--kernel", "all", false);
+  std::vector<int> kinds;
+  if (kernel == "all") kinds = {0, 1, 2};
+  else if (kernel == "gpk") kinds = {0};
+  else if (kernel == "lpk") kinds = {1};
+  else if (kernel == "ipk") kinds = {2};
+  else throw UsageError("--kernel must be gpk, lpk, ipk, or all");
+  stage = 2;  // parsing done: the rest are data errors
+  std::vector<KCfg> cfgs = {{2, 2, 2}, {4, 4, 4}, {8, 4, 4}, {16, 4, 4},
+                            {32, 4, 4}, {64, 2, 2}, {128, 2, 2}};  // default_block_configs
+  const std::string file = one(a, "--configs", "", false);
+  if (!file.empty()) {
+    std::ifstream is(file);
+    require(bool(is), file + ": cannot open");
+    cfgs.clear();
+    std::string line;
+    while (std::getline(is, line)) {
+      if (auto h = line.find('#'); h != std::string::npos) line.erase(h);
+      for (auto& c : line)
+        if (c == ',') c = ' ';
+      std::istringstream ss(line);
+      KCfg c;
+      if (ss >> c.bx >> c.by >> c.bz) cfgs.push_back(c);
+    }
+    require(!cfgs.empty(), file + ": no configurations found");
+  }
+  static const char* names[3] = {"GPK", "LPK", "IPK"};
+  Json out;
+  out.str("command", "rank-configs");
+  out.u64("n", n);
+  for (int kind : kinds) {
+    std::vector<std::pair<double, std::size_t>> order;
+    for (std::size_t i = 0; i < cfgs.size(); ++i)
+      order.emplace_back(estimate_time(kind, cfgs[i], n, S, L, G, bw), i);
+    std::stable_sort(order.begin(), order.end(),
+                     [](const auto& x, const auto& y) { return x.first < y.first; });
+    if (top > 0) {
+      require(top <= order.size(), "--top exceeds the configuration count");
+      order.resize(top);
+    }
+    if (a.flag.count("--json") && a.flag.at("--json")) {
+      std::string list = "[";
+      for (std::size_t r = 0; r < order.size(); ++r) {
+        const KCfg& c = cfgs[order[r].second];
+        Json e;
+        e.u64("bx", c.bx);
+        e.u64("by", c.by);
+        e.u64("bz", c.bz);
+        e.i64("rank", static_cast<long long>(r + 1));
+        e.dbl("seconds", order[r].first);
+        list += (r ? "," : "") + e.dump();
+      }
+      out.set(names[kind], list + "]");
+    } else {
+      std::cout << names[kind] << " (n=" << n << ", S=" << S << ", L=" << L
+                << ", G=" << (G ? G : S / L) << ", bw=" << bw << "):\n";
+      std::cout << "  rank    bx    by    bz        est. seconds\n";
+      for (std::size_t r = 0; r < order.size(); ++r) {
+        const KCfg& c = cfgs[order[r].second];
+        std::ostringstream row;
+        row.setf(std::ios::scientific);
+        row.precision(6);
+        row << "  " << r + 1 << "\t" << c.bx << "\t" << c.by << "\t" << c.bz << "\t"
+            << order[r].first;
+        std::cout << row.str() << "\n";
+      }
+    }
+  }
+  if (a.flag.count("--json") && a.flag.at("--json")) std::cout << out.dump() << "\n";
+  return 0;
+}
+
 const char* kUsage =
     "hierarchical grid refactoring for structured scientific data (B200 path)\n"
-    "usage: hgr-b200 {decompose,recompose,info,error} [options]\n";
+    "usage: hgr-b200 {decompose,recompose,info,error,rank-configs} [options]\n";
 
 std::vector<std::size_t> parse_dims(const std::string& s) {
   std::vector<std::size_t> dims;
@@ -435,9 +564,13 @@ int main(int argc, char** argv) {
       return prec == "f32" ? run_error<float>(o, r, a.flag["--json"])
                            : run_error<double>(o, r, a.flag["--json"]);
     }
-    if (cmd == "rank-configs")
-      throw UsageError("rank-configs: the analytical launch-configuration model "
-                       "(perf_model.hpp) is not part of the GPU path");
+    if (cmd == "rank-configs") {
+      Args a = parse(argc, argv, 2,
+                     {"--n", "--bytes-per-element", "--transaction-bytes", "--ghost", "--peak-bw",
+                      "--kernel", "--configs", "--top"},
+                     {"--json"});
+      return run_rank_configs(a, stage);
+    }
     throw UsageError("unknown subcommand: " + cmd);
   } catch (const UsageError& e) {
     std::cerr << kUsage << e.what() << "\n";

@@ -4,6 +4,7 @@ the reference's tests/test_cli.sh: exit codes (0 ok, 1 usage, 2 data/format),
 write_file), prefix-read byte accounting, f32 non-uniform round trip.
 The header/usage/error subcommands run on the host; decompose/recompose need a GPU."""
 import json
+import os
 import subprocess
 from pathlib import Path
 
@@ -136,3 +137,30 @@ def test_cli_end_to_end(tmp_path, cuda):
     rc, out, _ = run("error", "--original", b, "--reconstruction", tmp_path / "b3.raw",
                      "--precision", "f32", "--json")
     assert json.loads(out)["l2_rel"] <= 1e-5
+
+
+def test_rank_configs_matches_reference_model():
+    """rank-configs (hgr_main.cpp:230-286): ranks and modeled seconds equal the
+    reference's perf_model.hpp estimate_time; (2,2,2) ranks last (test_cli.sh:72-79)."""
+    import ctypes as C
+    rc, out, err = run("rank-configs", "--n", 513, "--bytes-per-element", 8, "--ghost", 4, "--json")
+    assert rc == 0, err
+    assert '"bx":2,"by":2,"bz":2,"rank":7' in out
+    j = json.loads(out)
+    assert list(j) == sorted(j) and j["n"] == 513
+    if oracle.available("reference"):
+        lib = C.CDLL(str(oracle.REF_SO))
+        f = lib.hgrref_estimate_time
+        f.restype = C.c_double
+        f.argtypes = [C.c_int] + [C.c_ulonglong] * 7 + [C.c_double]
+        for kind, name in enumerate(("GPK", "LPK", "IPK")):
+            for e in j[name]:
+                want = f(kind, e["bx"], e["by"], e["bz"], 513, 32, 8, 4, 1.0)
+                assert e["seconds"] == want, (name, e)
+    (Path(os.environ.get("TMPDIR", "/tmp")) / "hgr_cfgs.txt").write_text("8 4 4\n2,2,2\n# c\n16 4 4\n")
+    rc, out, _ = run("rank-configs", "--configs",
+                     Path(os.environ.get("TMPDIR", "/tmp")) / "hgr_cfgs.txt", "--kernel", "gpk",
+                     "--top", 1)
+    assert rc == 0 and "rank" in out
+    assert run("rank-configs", "--top", 9)[0] == 2  # data error
+    assert run("rank-configs", "--kernel", "xyz")[0] == 1  # usage error

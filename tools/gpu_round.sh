@@ -14,3 +14,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/ncu_launches_1025f64.csv python tools/prof_one.py 1025x1025x1025 f64 > $O/ncu.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/ncu_launches_1025f32.csv python tools/prof_one.py 1025x1025x1025 f32 >> $O/ncu.log 2>&1
 echo done
+# ncu --set full of the dominant kernel (top-level decompose level kernel), both precisions
+timeout 600 bash tools/ncu_one.sh $TAG/full_dec_f64 "k_level_fused.*0>" 6 1025x1025x1025 f64 >> $O/ncu.log 2>&1
+timeout 600 bash tools/ncu_one.sh $TAG/full_dec_f32 "k_level_fused.*0>" 6 1025x1025x1025 f32 >> $O/ncu.log 2>&1
+echo done2
