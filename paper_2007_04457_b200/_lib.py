@@ -9,7 +9,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhgr_b200.so"
+import os
+
+# HGR_B200_LIB: load another build of the same library (A/B timing of variants)
+LIB_PATH = Path(os.environ.get("HGR_B200_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libhgr_b200.so")
 
 HGR_OK, HGR_ERR_INVALID, HGR_ERR_CUDA, HGR_ERR_NONFINITE, HGR_ERR_NOMEM = 0, 1, 2, 3, 4
 HGR_F32, HGR_F64 = 0, 1

@@ -302,26 +302,31 @@ __global__ void __launch_bounds__(32 * kLW, 1)
 
 // ---- contiguous rows (dim 2) --------------------------------------------------------
 
-template <class T, int CH, int R>
+template <class T, int CH, int R, bool STAGE>
 struct RowsCfg {
   static constexpr int NT = 512, NW = NT / 32;
   static constexpr int CPW = 32 / R;         // chunks per warp
   static constexpr int NC = NW * CPW;        // chunks per row
   static constexpr int NP = NC * CH;
-  // the tile holds R rows of n; the last row's padded chunk positions read up to NP past its start
+  // a tile holds R rows of n; the last row's padded chunk positions read up to NP past its start
   static __host__ __device__ size_t buf_elems(int n) {
     return (size_t(R - 1) * n + (NP > n ? NP : n) + 15) / 16 * 16;
   }
+  // two input tiles (loads double-buffered) and, with STAGE, one output staging tile
   static size_t smem(int n) {
-    return (size_t(5) * NP + size_t(2) * NC * R + 2 * buf_elems(n)) * sizeof(T) + 16 + 2 * 8;
+    return (size_t(5) * NP + size_t(2) * NC * R + (STAGE ? 3 : 2) * buf_elems(n)) * sizeof(T) +
+           16 + 2 * 8;
   }
 };
 
-template <class T, int CH, int R>
+// STAGE: results go to a separate staging tile, so an input tile is refilled as
+// soon as its rows are in registers; otherwise results go back into the input
+// tile, which is refilled once the bulk store has read it (less shared memory).
+template <class T, int CH, int R, bool STAGE>
 __global__ void __launch_bounds__(512, 1)
     k_thomas_rows(const T* in, T* out, int64_t rows, int n, const T* __restrict__ mult,
                   const T* __restrict__ rpiv, const T* __restrict__ upper) {
-  using C = RowsCfg<T, CH, R>;
+  using C = RowsCfg<T, CH, R, STAGE>;
   constexpr int NC = C::NC, NP = C::NP, CPW = C::CPW;
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
@@ -334,13 +339,14 @@ __global__ void __launch_bounds__(512, 1)
   const size_t BE = C::buf_elems(n);
   T* buf0 = reinterpret_cast<T*>(
       (reinterpret_cast<uintptr_t>(sb + NC * R) + 15) & ~uintptr_t(15));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(buf0 + 2 * BE);
+  T* ot = buf0 + 2 * BE;  // output staging tile (STAGE)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(buf0 + (STAGE ? 3 : 2) * BE);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int r = lane % R, q = w * CPW + lane / R, s0 = q * CH;
   const int64_t ngroups = (rows + R - 1) / R;
 
-  // zero both tiles once: positions past a row's end then read finite data
-  for (size_t i = tid; i < 2 * BE; i += blockDim.x) buf0[i] = T(0);
+  // zero the tiles once: positions past a row's end then read finite data
+  for (size_t i = tid; i < (STAGE ? 3 : 2) * BE; i += blockDim.x) buf0[i] = T(0);
   build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
   if (tid == 0) {
     ptx::mbar_init(&bar[0], 1);
@@ -360,43 +366,47 @@ __global__ void __launch_bounds__(512, 1)
     ptx::bulk_g2s(buf0 + b * BE, in + g * R * int64_t(n), by, &bar[b]);
   };
   int64_t g = blockIdx.x;
+  const int64_t G = gridDim.x;
   if (tid == 0) {
     if (g < ngroups) load(g, 0);
-    if (g + gridDim.x < ngroups) load(g + gridDim.x, 1);
+    if (g + G < ngroups) load(g + G, 1);
   }
-  for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
+  for (int it = 0; g < ngroups; g += G, ++it) {
     const int b = it & 1;
-    T* tile = buf0 + b * BE;
     ptx::mbar_wait(&bar[b], uint32_t((it >> 1) & 1));
-    T* mine = tile + r * n + s0;
+    const T* mine = buf0 + b * BE + r * n + s0;
     T x[CH];
 #pragma unroll
     for (int k = 0; k < CH; ++k) x[k] = mine[k];
 
     sf[q * R + r] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
     __syncthreads();
+    // every thread has read its chunk: the input tile takes group g + 2G
+    if (STAGE && tid == 0 && g + 2 * G < ngroups) load(g + 2 * G, b);
     T c = T(0);
     for (int v = q > scan_depth<T, CH>() ? q - scan_depth<T, CH>() : 0; v < q; ++v)
       c = sf[v * R + r] + tP[v * CH + CH - 1] * c;
     ChunkSolve<T, CH>::apply(x, tP + s0, c);
     sb[q * R + r] = ChunkSolve<T, CH>::bwd_local(x, tu + s0, tp + s0);
+    if (STAGE && tid == 0) ptx::bulk_wait_read0();  // the previous store has read `ot`
     __syncthreads();
     c = T(0);
     for (int v = q + scan_depth<T, CH>() < NC - 1 ? q + scan_depth<T, CH>() : NC - 1; v > q; --v)
       c = sb[v * R + r] + tQ[v * CH] * c;
     ChunkSolve<T, CH>::apply(x, tQ + s0, c);
 
+    T* dst = (STAGE ? ot : buf0 + b * BE) + r * n + s0;
 #pragma unroll
     for (int k = 0; k < CH; ++k)
-      if (s0 + k < n) mine[k] = x[k];
+      if (s0 + k < n) dst[k] = x[k];
     ptx::fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      ptx::bulk_s2g(out + g * R * int64_t(n), tile, gbytes(g));
+      ptx::bulk_s2g(out + g * R * int64_t(n), STAGE ? ot : buf0 + b * BE, gbytes(g));
       ptx::bulk_commit();
-      if (g + 2 * int64_t(gridDim.x) < ngroups) {
+      if (!STAGE && g + 2 * G < ngroups) {
         ptx::bulk_wait_read0();  // the store has read the tile; refill it
-        load(g + 2 * int64_t(gridDim.x), b);
+        load(g + 2 * G, b);
       }
     }
   }
@@ -430,9 +440,10 @@ void set_smem_attr(const void* fn, size_t bytes) {
 template <class T, int CH, int R>
 void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const T* rpiv,
               const T* upper, cudaStream_t s) {
-  using C = RowsCfg<T, CH, R>;
+  constexpr bool STAGE = sizeof(T) == 4;  // fp64's 16-row tiles leave no room for a third
+  using C = RowsCfg<T, CH, R, STAGE>;
   const size_t smem = C::smem(int(n));
-  auto kern = k_thomas_rows<T, CH, R>;
+  auto kern = k_thomas_rows<T, CH, R, STAGE>;
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int64_t groups = (rows + R - 1) / R;
   const int grid = int(groups < sm_count() ? groups : sm_count());
@@ -476,13 +487,21 @@ bool launch_thomas_fast(const T* in, T* out, const int64_t e[3], int dim, const 
     if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
       return false;
     const int64_t rows = e[0] * e[1];
-    if (n <= 32 * 2) run_rows<T, 2, 16>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 5) run_rows<T, 5, 16>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 9) run_rows<T, 9, 16>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 32 * 17) run_rows<T, 17, 16>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (sizeof(T) == 4 && n <= 32 * 33) run_rows<T, 33, 16>(in, out, rows, n, mult, rpiv, upper, s);
-    else if (n <= 64 * 17) run_rows<T, 17, 8>(in, out, rows, n, mult, rpiv, upper, s);
-    else return false;
+    if constexpr (sizeof(T) == 8) {
+      if (n <= 32 * 2) run_rows<T, 2, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 5) run_rows<T, 5, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 9) run_rows<T, 9, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 17) run_rows<T, 17, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 64 * 17) run_rows<T, 17, 8>(in, out, rows, n, mult, rpiv, upper, s);
+      else return false;
+    } else {
+      if (n <= 32 * 2) run_rows<T, 2, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 5) run_rows<T, 5, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 9) run_rows<T, 9, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 17) run_rows<T, 17, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else if (n <= 32 * 33) run_rows<T, 33, 16>(in, out, rows, n, mult, rpiv, upper, s);
+      else return false;
+    }
     return true;
   }
   if (e[0] * e[1] * e[2] >= (int64_t(1) << 31)) return false;  // 32-bit offsets
