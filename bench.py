@@ -256,10 +256,15 @@ def run_gpu(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; HGR_BENCH_BACKEND=gloo lets several ranks share one GPU
+    # (a functional check of the multi-rank path on a single-GPU box)
+    backend = os.environ.get("HGR_BENCH_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
+    red_dev = dev if backend == "nccl" else None
 
     shape, dt = cfg["shape"], cfg["dtype"]
     coords = coords_for(shape, cfg["nonuniform"])
@@ -316,7 +321,7 @@ def run_gpu(args, cfg):
     plan.set_profiling(False)
     launches_step = plan.launches(0, L) + plan.launches(1, L)
 
-    ms_max, chk_sum = reduce_across_ranks(ms_step, float(x.double().sum().item()), dev)
+    ms_max, chk_sum = reduce_across_ranks(ms_step, float(x.double().sum().item()), red_dev)
     value = world * 2 * nbytes / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API: pinned host field -> device, full
@@ -338,7 +343,7 @@ def run_gpu(args, cfg):
         err_h = err_d.to("cpu", non_blocking=False)
     eb.record(stream)
     torch.cuda.synchronize(dev)
-    e2e_ms, _ = reduce_across_ranks(ea.elapsed_time(eb) / e2e_steps, 0.0, dev)
+    e2e_ms, _ = reduce_across_ranks(ea.elapsed_time(eb) / e2e_steps, 0.0, red_dev)
     e2e_value = world * 2 * nbytes / (e2e_ms * 1e-3) / 1e9
     del host, xin, yout
 
