@@ -31,7 +31,11 @@ void make_tma_1d(CUtensorMap* map, const void* base, uint64_t n, int elem_bytes,
   require(fn != nullptr, "cuTensorMapEncodeTiled is unavailable (driver too old?)");
   require((reinterpret_cast<uintptr_t>(base) & 15) == 0, "TMA base must be 16-byte aligned");
   require(box > 0 && box <= 256 && (box * elem_bytes) % 16 == 0, "TMA box size");
-  const cuuint64_t gdim[1] = {cuuint64_t(n)};
+  // a 1D map's extent must stay below 2^31 elements (larger extents are an illegal
+  // instruction at copy time, measured on B200); callers keep every box of a
+  // launch inside the first 2^31 - 1 elements from the base (run_fused / run_interp)
+  const uint64_t nmax = (uint64_t(1) << 31) - 1;
+  const cuuint64_t gdim[1] = {cuuint64_t(n < nmax ? n : nmax)};
   const cuuint64_t gstride[1] = {cuuint64_t(elem_bytes)};  // unused for rank 1
   const cuuint32_t bdim[1] = {cuuint32_t(box)};
   const cuuint32_t estr[1] = {1};
