@@ -52,6 +52,13 @@ CONFIGS = {
     "513sq_f64": dict(shape=(513, 513), dtype="f64", nonuniform=False,
                       workload="2D 513x513 fp64 uniform grid (BASELINE configs[0])",
                       sample=(513, 513)),
+    # not BASELINE configs: large 2D / 1D grids for tuning the 2D / 1D paths
+    "8193sq_f32": dict(shape=(8193, 8193), dtype="f32", nonuniform=False,
+                       workload="2D 8193x8193 fp32 uniform grid (extra, not in BASELINE)",
+                       sample=(1025, 1025)),
+    "line_f64": dict(shape=((1 << 26) + 1,), dtype="f64", nonuniform=False,
+                     workload="1D 2^26+1 fp64 uniform line (extra, not in BASELINE)",
+                     sample=((1 << 20) + 1,)),
 }
 DEFAULT_CONFIG = "weak1025f32"
 FALLBACK_HBM_GBS = 6650.0

@@ -67,6 +67,10 @@ template <class T>
 void launch_thomas(T* z, const int64_t ext[3], int dim, const T* mult, const T* rpiv,
                    const T* upper, T* apply, int sign, cudaStream_t s);
 
+// y[i] += sign * x[i], i < n
+template <class T>
+void launch_axpy(T* y, const T* x, int64_t n, int sign, cudaStream_t s);
+
 // dst[q] = src[q * stride] (3D), dst extents given.
 template <class T>
 void launch_gather(const T* src, const int64_t src_ext[3], int64_t stride, T* dst,

@@ -304,6 +304,14 @@ __global__ void k_fiber_thomas(const T* __restrict__ v, T* __restrict__ out, int
   }
 }
 
+// y[i] += sign * x[i] (coarse += / -= correction after a register-tiled Thomas pass)
+template <class T>
+__global__ void k_axpy(T* y, const T* x, int64_t n, int sign) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = sign > 0 ? y[i] + x[i] : y[i] - x[i];
+}
+
 // ---- launchers -----------------------------------------------------------------
 
 #define LAUNCH(kernel, work, threads, s, ...)                                   \
@@ -332,6 +340,10 @@ void launch_thomas(T* z, const int64_t e[3], int dim, const T* mult, const T* rp
                    const T* upper, T* apply, int sign, cudaStream_t s) {
   int64_t lines = e[0] * e[1] * e[2] / e[dim];
   LAUNCH(k_thomas<T>, lines, 128, s, z, e[0], e[1], e[2], dim, mult, rpiv, upper, apply, sign);
+}
+template <class T>
+void launch_axpy(T* y, const T* x, int64_t n, int sign, cudaStream_t s) {
+  LAUNCH(k_axpy<T>, n, 256, s, y, x, n, sign);
 }
 template <class T>
 void launch_gather(const T* src, const int64_t se[3], int64_t stride, T* dst,
@@ -388,6 +400,7 @@ void launch_fiber_thomas(const T* v, T* out, int64_t n, int64_t count, const T* 
                               cudaStream_t);                                                 \
   template void launch_thomas<T>(T*, const int64_t*, int, const T*, const T*, const T*, T*,  \
                                  int, cudaStream_t);                                         \
+  template void launch_axpy<T>(T*, const T*, int64_t, int, cudaStream_t);                    \
   template void launch_gather<T>(const T*, const int64_t*, int64_t, T*, const int64_t*,      \
                                  cudaStream_t);                                              \
   template void launch_scatter_even<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);     \

@@ -16,6 +16,11 @@ template <class T>
 bool launch_thomas_fast(const T* in, T* out, const int64_t ext[3], int dim, const T* mult,
                         const T* rpiv, const T* upper, cudaStream_t s);
 
+// True if the pass along `dim` cuts lines into overlapping windows; such a
+// pass must run out of place (in != out).
+template <class T>
+bool thomas_needs_out_of_place(const int64_t ext[3], int dim);
+
 enum FusedMode : int {
   kFusedDecompose = 0,  // coefficients -> coef_out, K*U -> zload
   kFusedLoadOnly = 1,   // K*U -> zload only

@@ -500,6 +500,8 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
 // first reduces the 3 fine columns (rows) next to the face with K2 (K1) for the
 // 5 fine planes of its coarse plane into shared memory, then every thread forms
 // its output from 25 of those sums.
+constexpr int kFaceSeg = 256;  // coarse outputs of faces 0/1 per CTA (2x fine for faces 2/3)
+
 template <class T, int MODE>
 __global__ void __launch_bounds__(256)
     k_level_face(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ zload,
@@ -515,9 +517,15 @@ __global__ void __launch_bounds__(256)
     const int i0 = blockIdx.x;
     if (i0 >= c0) return;
     const int ne = face == 0 ? e1 : e2;  // fine extent along the free dimension
+    // this CTA's outputs q0 .. q1-1 along the free dimension and their fine span
+    const int nout = face == 0 ? c1 : c2 - 1;
+    const int q0 = int(blockIdx.z) * kFaceSeg;
+    if (q0 >= nout) return;
+    const int q1 = min(nout, q0 + kFaceSeg);
+    const int f_lo = max(0, 2 * q0 - 2), W = min(ne, 2 * q1 + 1) - f_lo;
     // R[a][f] = sum over the 3 fine cells next to the face (K2 or K1 boundary row)
-    for (int idx = tid; idx < 5 * ne; idx += nt) {
-      const int x = idx / ne, f = idx - x * ne;
+    for (int idx = tid; idx < 5 * W; idx += nt) {
+      const int x = idx / W, f = f_lo + idx - x * W;
       const int f0 = 2 * i0 - 2 + x;
       T r = T(0);
       if (f0 >= 0 && f0 < e0) {
@@ -536,8 +544,7 @@ __global__ void __launch_bounds__(256)
       Rs[idx] = r;
     }
     __syncthreads();
-    const int nout = face == 0 ? c1 : c2 - 1;
-    for (int q = tid; q < nout; q += nt) {
+    for (int q = q0 + tid; q < q1; q += nt) {
       T acc = T(0);
       for (int x = 0; x < 5; ++x) {
         const int f0 = 2 * i0 - 2 + x;
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(256)
           const int f = 2 * q - 2 + y;
           if (f < 0 || f >= ne) continue;
           const T w = face == 0 ? a.taps[1][int64_t(q) * 5 + y] : a.taps[2][int64_t(q) * 5 + y];
-          acc1 += w * Rs[x * ne + f];
+          acc1 += w * Rs[x * W + f - f_lo];
         }
         acc += w0 * acc1;
       }
@@ -566,8 +573,11 @@ __global__ void __launch_bounds__(256)
     return U[(2 * b0) * plane + (2 * b1) * e2 + 2 * b2];
   };
   const int n = face == 2 ? e1 : e2 - 1;
+  const int q0 = int(blockIdx.z) * 2 * kFaceSeg;
+  if (q0 >= n) return;
+  const int q1 = min(n, q0 + 2 * kFaceSeg);
   bool bad = false;
-  for (int q = tid; q < n; q += nt) {
+  for (int q = q0 + tid; q < q1; q += nt) {
     const int r = face == 2 ? q : e1 - 1, c = face == 2 ? e2 - 1 : q;
     const int64_t idx = j * plane + int64_t(r) * e2 + c;
     const T u = U[idx];
@@ -633,8 +643,10 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
     HGR_CUDA_CHECK(cudaGetLastError());
     sa = sb;
   }
-  const dim3 fgrid(unsigned(std::max(a.c[0], a.e[0])), MODE == kFusedDecompose ? 4 : 2);
-  const size_t fsmem = size_t(5) * size_t(std::max(a.e[1], a.e[2])) * sizeof(T);
+  const int64_t fseg = (std::max(a.e[1], a.e[2]) + 2 * kFaceSeg - 1) / (2 * kFaceSeg) + 1;
+  const dim3 fgrid(unsigned(std::max(a.c[0], a.e[0])), MODE == kFusedDecompose ? 4 : 2,
+                   unsigned(fseg));
+  const size_t fsmem = size_t(5) * size_t(2 * kFaceSeg + 3) * sizeof(T);
   set_level_face_smem<T, MODE>(fsmem);
   k_level_face<T, MODE><<<fgrid, 256, fsmem, s>>>(U, coef, z, gather, a, flag);
   HGR_CUDA_CHECK(cudaGetLastError());

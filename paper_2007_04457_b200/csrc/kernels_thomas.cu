@@ -36,14 +36,17 @@ namespace {
 //   tm[i] = m_{i-1} (0 at i = 0 and i >= n), tp[i] = 1/p_i, tu[i] = u_i (0 at
 //   i >= n-1), P (forward carry products), Q (backward carry products);
 //   positions >= n have tp = 0 so padding never feeds back.
+//   With a window start ws the tables cover line positions ws .. ws+NP-1
+//   (positions outside the line are padding).
 template <class T>
 __device__ void build_tables(T* tm, T* tP, T* tp, T* tu, T* tQ, int n, int NC, int CH,
-                             const T* mult, const T* rpiv, const T* upper) {
+                             const T* mult, const T* rpiv, const T* upper, int ws = 0) {
   const int NP = NC * CH;
   for (int i = threadIdx.x; i < NP; i += blockDim.x) {
-    tm[i] = (i >= 1 && i < n) ? mult[i - 1] : T(0);
-    tp[i] = i < n ? rpiv[i] : T(0);
-    tu[i] = i < n - 1 ? upper[i] : T(0);
+    const int pos = ws + i;
+    tm[i] = (pos >= 1 && pos < n) ? mult[pos - 1] : T(0);
+    tp[i] = (pos >= 0 && pos < n) ? rpiv[pos] : T(0);
+    tu[i] = (pos >= 0 && pos < n - 1) ? upper[pos] : T(0);
   }
   __syncthreads();
   for (int q = threadIdx.x; q < NC; q += blockDim.x) {
@@ -147,12 +150,22 @@ constexpr int kLW = 16;  // warps (= chunks per line) of k_thomas_lines
 // other strided dim; the c2 % W remaining columns form "tail" groups whose
 // threads take W consecutive ia at one column. All offsets are 32-bit (the
 // launcher requires < 2^31 elements).
-template <class T, int CH, int LPT, bool RP>
+// WIN (lines longer than one group's NP positions): a line is cut into windows
+// of NP positions overlapping by 2*H (see k_thomas_long below); groups are
+// (window, line group) pairs, window-major, and the tables are rebuilt when a
+// CTA moves to another window. The window start ws shifts every position.
+template <class T>
+constexpr int window_halo() {
+  return sizeof(T) == 8 ? 56 : 26;
+}
+
+template <class T, int CH, int LPT, bool RP, bool WIN>
 __global__ void __launch_bounds__(32 * kLW, 1)
     k_thomas_lines(const T* in, T* out, int n, int sd, int so, int na, int c2, int nfull,
-                   int ntail, int ngroups, const T* __restrict__ mult, const T* __restrict__ rpiv,
-                   const T* __restrict__ upper) {
+                   int ntail, int nlg, int S, int J, const T* __restrict__ mult,
+                   const T* __restrict__ rpiv, const T* __restrict__ upper) {
   constexpr int NT = 32 * kLW, NC = kLW, NP = NC * CH, GW = 32 * LPT;
+  constexpr int H = window_halo<T>();
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
   T* tP = tm + NP;
@@ -162,26 +175,47 @@ __global__ void __launch_bounds__(32 * kLW, 1)
   T* sf = tQ + NP;         // [NC][GW] forward chunk summaries
   T* sb = sf + NC * GW;    // [NC][GW] backward chunk summaries
   T* land = sb + NC * GW;  // [CH][NT][LPT] per-thread landing zone
-  build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
+  if (!WIN) build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s0 = w * CH;
-  const int kmax = n - s0 < CH ? n - s0 : CH;  // valid positions of this warp's chunk
+  const int kmax = n - s0 < CH ? n - s0 : CH;  // valid positions of this warp's chunk (!WIN)
   const int nfull_groups = na * nfull;
+  const int ngroups = WIN ? nlg * J : nlg;
+  // window of group g (WIN): start position, owned positions [lo, hi)
+  auto wstart = [&](int g) { return WIN && J > 1 ? (g / nlg) * S - H : 0; };
 
-  // offset of position s0 of line u of this thread in group g (-1: no line);
-  // full groups: lines adjacent (offset + u), tail groups: offset + u*so
-  auto line_off = [&](int g, int u) {
-    if (g < nfull_groups) {
-      const int ia = int(unsigned(g) / unsigned(nfull)), ib = g - ia * nfull;
-      return ia * so + ib * GW + LPT * lane + u + s0 * sd;
+  // offset of position 0 of line u of this thread in line group lg (-1: no
+  // line); full groups: lines adjacent (offset + u), tail groups: offset + u*so
+  auto line_base = [&](int lg, int u) {
+    if (lg < nfull_groups) {
+      const int ia = int(unsigned(lg) / unsigned(nfull)), ib = lg - ia * nfull;
+      return ia * so + ib * GW + LPT * lane + u;
     }
-    const int t = g - nfull_groups;  // tail: GW rows ia at column c2 - ntail + (t % ntail)
+    const int t = lg - nfull_groups;  // tail: GW rows ia at column c2 - ntail + (t % ntail)
     const int ia = (t / ntail) * GW + LPT * lane + u, col = c2 - ntail + t % ntail;
-    return ia < na ? ia * so + col + s0 * sd : -1;
+    return ia < na ? ia * so + col : -1;
+  };
+  // offset of position s0 of line u in group g (!WIN)
+  auto line_off = [&](int g, int u) {
+    const int b = line_base(g, u);
+    return b < 0 ? -1 : b + s0 * sd;
   };
   auto prefetch = [&](int g) {
     T* ld = land + tid * LPT;
-    if (g < nfull_groups) {
+    if constexpr (WIN) {
+      const int lg = g % nlg, p0 = wstart(g) + s0;
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) {
+        const int off = line_base(lg, u);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int p = p0 + k;
+          const bool ok = off >= 0 && p >= 0 && p < n;
+          ptx::cp_async_elem<int(sizeof(T))>(ld + k * NT * LPT + u, in + (ok ? off + p * sd : 0),
+                                             ok ? int(sizeof(T)) : 0);
+        }
+      }
+    } else if (g < nfull_groups) {
       const T* src = in + line_off(g, 0);
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
@@ -211,12 +245,21 @@ __global__ void __launch_bounds__(32 * kLW, 1)
   // into a second register set instead of the shared-memory landing zone
   T nx[RP ? CH : 1];
   auto prefetch_regs = [&](int g) {
-    const int off = line_off(g, 0);
-    const T* src = in + (off < 0 ? 0 : off);
+    if constexpr (WIN) {
+      const int off = line_base(g % nlg, 0), p0 = wstart(g) + s0;
 #pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      nx[k] = (off >= 0 && k < kmax) ? __ldg(src) : T(0);
-      if (k + 1 < kmax) src += sd;
+      for (int k = 0; k < CH; ++k) {
+        const int p = p0 + k;
+        nx[k] = (off >= 0 && p >= 0 && p < n) ? __ldg(in + off + p * sd) : T(0);
+      }
+    } else {
+      const int off = line_off(g, 0);
+      const T* src = in + (off < 0 ? 0 : off);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        nx[k] = (off >= 0 && k < kmax) ? __ldg(src) : T(0);
+        if (k + 1 < kmax) src += sd;
+      }
     }
   };
   int g = blockIdx.x;
@@ -224,7 +267,16 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     if constexpr (RP) prefetch_regs(g);
     else prefetch(g);
   }
+  int cur_w = -1;
   for (; g < ngroups; g += gridDim.x) {
+    if constexpr (WIN) {
+      const int wi = g / nlg;
+      if (wi != cur_w) {  // every thread is past the previous group's table reads
+        cur_w = wi;
+        __syncthreads();
+        build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper, wstart(g));
+      }
+    }
     T x[LPT][CH];
     if constexpr (RP) {
 #pragma unroll
@@ -274,7 +326,20 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     }
     ChunkSolve<T, CH, LPT>::apply(x, tQ + s0, c);
 
-    if (g < nfull_groups) {
+    if constexpr (WIN) {
+      const int wi = g / nlg, ws = wstart(g), p0 = ws + s0;
+      const int lo = J > 1 ? wi * S : 0, hi = J > 1 && wi * S + S < n ? wi * S + S : n;
+#pragma unroll
+      for (int u = 0; u < LPT; ++u) {
+        const int off = line_base(g % nlg, u);
+        if (off < 0) continue;
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          const int p = p0 + k;
+          if (p >= lo && p < hi) out[off + p * sd] = x[u][k];
+        }
+      }
+    } else if (g < nfull_groups) {
       T* dst = out + line_off(g, 0);
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
@@ -413,6 +478,124 @@ __global__ void __launch_bounds__(512, 1)
   if (tid == 0) ptx::bulk_wait0();
 }
 
+// ---- long contiguous rows (dim 2, rows beyond the row tiles) ------------------------
+//
+// A row is cut into windows of NP = 512*CH positions that overlap by 2*H: the
+// carry into a window from outside it is dropped, which the damping bound above
+// makes invisible (< 2^-B) once H >= B positions away from the window's edges,
+// so only the window's middle [H, NP-H) is stored (the whole row when it fits
+// one window). Groups = (window, row) pairs, window-major, so a CTA keeps one
+// window's per-position factors in registers across consecutive rows.
+
+template <class T, int CH>
+struct LongCfg {
+  static constexpr int NT = 512, NC = NT, NP = NC * CH;
+  static constexpr int TILE = NP + NC;  // one pad element per chunk: conflict-free chunk reads
+  static size_t smem() { return (size_t(2) * TILE + size_t(4) * NC) * sizeof(T); }
+};
+
+template <class T, int CH>
+__global__ void __launch_bounds__(512, 1)
+    k_thomas_long(const T* in, T* out, int64_t rows, int64_t n, int64_t S, int64_t J,
+                  const T* __restrict__ mult, const T* __restrict__ rpiv,
+                  const T* __restrict__ upper) {
+  using C = LongCfg<T, CH>;
+  constexpr int NT = C::NT, NC = C::NC, TILE = C::TILE;
+  constexpr int H = window_halo<T>();
+  extern __shared__ __align__(16) unsigned char smem_t[];
+  T* tile = reinterpret_cast<T*>(smem_t);  // [2][TILE]
+  T* sf = tile + 2 * TILE;                 // [NC] forward chunk summaries
+  T* sb = sf + NC;                         // [NC] backward chunk summaries
+  T* sP = sb + NC;                         // [NC] forward chunk products
+  T* sQ = sP + NC;                         // [NC] backward chunk products
+  const int tid = threadIdx.x, q = tid, s0 = q * CH;
+  const int64_t ngroups = rows * J;
+  auto wstart = [&](int64_t j) { return J == 1 ? int64_t(0) : j * S - H; };
+  auto prefetch = [&](int64_t g, int b) {
+    const int64_t j = g / rows, r = g - j * rows, ws = wstart(j);
+    const T* row = in + r * n;
+    T* t = tile + b * TILE;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int i = k * NT + tid;
+      const int64_t pos = ws + i;
+      const bool ok = pos >= 0 && pos < n;
+      ptx::cp_async_elem<int(sizeof(T))>(t + i + i / CH, row + (ok ? pos : 0),
+                                         ok ? int(sizeof(T)) : 0);
+    }
+    ptx::cp_async_commit();
+  };
+
+  T tm[CH], tp[CH], tu[CH];
+  int64_t cur_j = -1;
+  int64_t g = blockIdx.x;
+  if (g < ngroups) prefetch(g, 0);
+  for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int64_t j = g / rows, r = g - j * rows, ws = wstart(j);
+    if (j != cur_j) {  // this window's factors; padding positions never feed back
+      cur_j = j;
+      T a = T(1), c = T(1);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int64_t pos = ws + s0 + k;
+        tm[k] = (pos >= 1 && pos < n) ? mult[pos - 1] : T(0);
+        tp[k] = (pos >= 0 && pos < n) ? rpiv[pos] : T(0);
+        tu[k] = (pos >= 0 && pos < n - 1) ? upper[pos] : T(0);
+        a *= -tm[k];
+        c *= -(tu[k] * tp[k]);
+      }
+      sP[q] = a;  // read by the scans after the barrier below
+      sQ[q] = c;
+    }
+    ptx::cp_async_wait_all();
+    __syncthreads();  // tile b complete; the previous group's store has read tile b^1
+    if (g + int64_t(gridDim.x) < ngroups) prefetch(g + gridDim.x, b ^ 1);
+    T* t = tile + b * TILE;
+    T x[CH];
+#pragma unroll
+    for (int k = 0; k < CH; ++k) x[k] = t[s0 + q + k];  // padded index i + i / CH
+
+    // forward: local solve, truncated exact carry scan, running-product apply
+    sf[q] = ChunkSolve<T, CH>::fwd_local(x, tm);
+    __syncthreads();
+    T c = T(0);
+    for (int v = q > scan_depth<T, CH>() ? q - scan_depth<T, CH>() : 0; v < q; ++v)
+      c = sf[v] + sP[v] * c;
+    {
+      T p = T(1);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        p *= -tm[k];
+        x[k] += p * c;
+      }
+    }
+    // backward
+    sb[q] = ChunkSolve<T, CH>::bwd_local(x, tu, tp);
+    __syncthreads();
+    c = T(0);
+    for (int v = q + scan_depth<T, CH>() < NC - 1 ? q + scan_depth<T, CH>() : NC - 1; v > q; --v)
+      c = sb[v] + sQ[v] * c;
+    {
+      T p = T(1);
+#pragma unroll
+      for (int k = CH - 1; k >= 0; --k) {
+        p *= -(tu[k] * tp[k]);
+        x[k] += p * c;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CH; ++k) t[s0 + q + k] = x[k];
+    __syncthreads();
+    // coalesced store of the window's owned positions
+    const int lo = J == 1 ? 0 : H;
+    const int64_t hi64 = J == 1 ? n : (j * S + S < n ? j * S + S : n) - ws;
+    const int hi = int(hi64);
+    T* orow = out + r * n + ws;
+    for (int i = lo + tid; i < hi; i += NT) orow[i] = t[i + i / CH];
+  }
+}
+
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -451,7 +634,7 @@ void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const
   HGR_CUDA_CHECK(cudaGetLastError());
 }
 
-template <class T, int CH>
+template <class T, int CH, bool WIN>
 void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, const T* rpiv,
                const T* upper, cudaStream_t s) {
   // fp32: the next group's chunk is prefetched into registers (fp64 chunks are
@@ -461,7 +644,7 @@ void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, 
   constexpr int NT = 32 * kLW, NP = kLW * CH, GW = 32 * LPT;
   const size_t smem =
       (size_t(5) * NP + 2 * kLW * GW + (RP ? 0 : size_t(CH) * NT * LPT)) * sizeof(T);
-  auto kern = k_thomas_lines<T, CH, LPT, RP>;
+  auto kern = k_thomas_lines<T, CH, LPT, RP, WIN>;
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int n = int(e[dim]);
   const int sd = int(dim == 0 ? e[1] * e[2] : e[2]);
@@ -469,13 +652,50 @@ void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, 
   const int na = int(dim == 0 ? e[1] : e[0]);
   const int c2 = int(e[2]);
   const int nfull = c2 / GW, ntail = c2 % GW;
-  const int groups = na * nfull + ((na + GW - 1) / GW) * ntail;
-  const int grid = groups < sm_count() ? groups : sm_count();
-  kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, na, c2, nfull, ntail, groups, mult, rpiv, upper);
+  const int nlg = na * nfull + ((na + GW - 1) / GW) * ntail;
+  const int S = n <= NP ? n : NP - 2 * window_halo<T>();
+  const int J = (n + S - 1) / S;
+  const int64_t groups = int64_t(nlg) * J;
+  const int grid = int(groups < sm_count() ? groups : sm_count());
+  kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, na, c2, nfull, ntail, nlg, S, J, mult, rpiv,
+                              upper);
   HGR_CUDA_CHECK(cudaGetLastError());
 }
 
+template <class T, int CH>
+void run_long(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const T* rpiv,
+              const T* upper, cudaStream_t s) {
+  using C = LongCfg<T, CH>;
+  const int64_t S = n <= C::NP ? n : C::NP - 2 * window_halo<T>();
+  const int64_t J = (n + S - 1) / S;
+  auto kern = k_thomas_long<T, CH>;
+  set_smem_attr(reinterpret_cast<const void*>(kern), C::smem());
+  const int64_t groups = rows * J;
+  const int grid = int(groups < sm_count() ? groups : sm_count());
+  kern<<<grid, C::NT, C::smem(), s>>>(in, out, rows, n, S, J, mult, rpiv, upper);
+  HGR_CUDA_CHECK(cudaGetLastError());
+}
+
+// longest rows of the register-tiled row kernels; longer rows take k_thomas_long
+template <class T>
+constexpr int64_t rows_max() {
+  return sizeof(T) == 8 ? 64 * 17 : 32 * 33;
+}
+constexpr int kLinesMaxCH = 33;
+// long rows: fp64 chunks of 8, fp32 chunks of 16 (512 chunks per window)
+template <class T>
+constexpr int long_ch() {
+  return sizeof(T) == 8 ? 8 : 16;
+}
+
 }  // namespace
+
+template <class T>
+bool thomas_needs_out_of_place(const int64_t e[3], int dim) {
+  const int64_t n = e[dim];
+  if (dim == 2) return n > rows_max<T>() && n > int64_t(512) * long_ch<T>();
+  return n > int64_t(kLW) * kLinesMaxCH;
+}
 
 template <class T>
 bool launch_thomas_fast(const T* in, T* out, const int64_t e[3], int dim, const T* mult,
@@ -483,37 +703,46 @@ bool launch_thomas_fast(const T* in, T* out, const int64_t e[3], int dim, const 
   const int64_t n = e[dim];
   if (n < 2) return false;
   if (dim == 2) {
+    const int64_t rows = e[0] * e[1];
+    if (n > rows_max<T>()) {
+      require(in != out || !thomas_needs_out_of_place<T>(e, dim),
+              "windowed Thomas pass must run out of place");
+      run_long<T, long_ch<T>()>(in, out, rows, n, mult, rpiv, upper, s);
+      return true;
+    }
     // bulk copies need 16-byte aligned group blocks
     if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
       return false;
-    const int64_t rows = e[0] * e[1];
     if constexpr (sizeof(T) == 8) {
       if (n <= 32 * 2) run_rows<T, 2, 16>(in, out, rows, n, mult, rpiv, upper, s);
       else if (n <= 32 * 5) run_rows<T, 5, 16>(in, out, rows, n, mult, rpiv, upper, s);
       else if (n <= 32 * 9) run_rows<T, 9, 16>(in, out, rows, n, mult, rpiv, upper, s);
       else if (n <= 32 * 17) run_rows<T, 17, 16>(in, out, rows, n, mult, rpiv, upper, s);
-      else if (n <= 64 * 17) run_rows<T, 17, 8>(in, out, rows, n, mult, rpiv, upper, s);
-      else return false;
+      else run_rows<T, 17, 8>(in, out, rows, n, mult, rpiv, upper, s);
     } else {
       if (n <= 32 * 2) run_rows<T, 2, 16>(in, out, rows, n, mult, rpiv, upper, s);
       else if (n <= 32 * 5) run_rows<T, 5, 16>(in, out, rows, n, mult, rpiv, upper, s);
       else if (n <= 32 * 9) run_rows<T, 9, 16>(in, out, rows, n, mult, rpiv, upper, s);
       else if (n <= 32 * 17) run_rows<T, 17, 16>(in, out, rows, n, mult, rpiv, upper, s);
-      else if (n <= 32 * 33) run_rows<T, 33, 16>(in, out, rows, n, mult, rpiv, upper, s);
-      else return false;
+      else run_rows<T, 33, 16>(in, out, rows, n, mult, rpiv, upper, s);
     }
     return true;
   }
   if (e[0] * e[1] * e[2] >= (int64_t(1) << 31)) return false;  // 32-bit offsets
-  if (n <= kLW * 2) run_lines<T, 2>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= kLW * 5) run_lines<T, 5>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= kLW * 9) run_lines<T, 9>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= kLW * 17) run_lines<T, 17>(in, out, e, dim, mult, rpiv, upper, s);
-  else if (n <= kLW * 33) run_lines<T, 33>(in, out, e, dim, mult, rpiv, upper, s);
-  else return false;
+  if (n <= kLW * 2) run_lines<T, 2, false>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 5) run_lines<T, 5, false>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 9) run_lines<T, 9, false>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * 17) run_lines<T, 17, false>(in, out, e, dim, mult, rpiv, upper, s);
+  else if (n <= kLW * kLinesMaxCH) run_lines<T, kLinesMaxCH, false>(in, out, e, dim, mult, rpiv, upper, s);
+  else {
+    require(in != out, "windowed Thomas pass must run out of place");
+    run_lines<T, kLinesMaxCH, true>(in, out, e, dim, mult, rpiv, upper, s);
+  }
   return true;
 }
 
+template bool thomas_needs_out_of_place<float>(const int64_t*, int);
+template bool thomas_needs_out_of_place<double>(const int64_t*, int);
 template bool launch_thomas_fast<float>(const float*, float*, const int64_t*, int, const float*,
                                         const float*, const float*, cudaStream_t);
 template bool launch_thomas_fast<double>(const double*, double*, const int64_t*, int,

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -274,11 +275,16 @@ class PlanT final : public Plan {
 
  private:
   void correction(int l, const T* in, T* z, T* apply, int sign, cudaStream_t s);
-  void thomas_all(int l, T* z, T* last_out, cudaStream_t s);
+  void thomas_all(int l, T* src, T* last_out, cudaStream_t s);
+  bool thomas_route(int l, const T* src, const T* last_out) const;
+  T* thomas_src(int l, T* last_out) const;
   void assemble(T* out, cudaStream_t s);
   static constexpr double sz() { return double(sizeof(T)); }
   void decompose_level(int l, const T* src, T* coef_dst, bool in_place, cudaStream_t s);
-  bool big(int l) const { return h.node_count(l) >= (std::size_t(1) << 15); }
+  // levels with at least big_nodes_ nodes run the fused / TMA kernels, smaller
+  // ones the one-thread-per-item kernels (tuning knob: HGR_BIG_LEVEL_NODES)
+  bool big(int l) const { return h.node_count(l) >= big_nodes_; }
+  std::size_t big_nodes_ = std::size_t(1) << 15;
   int L() const { return h.L; }
 
   std::vector<LevelArgs<T>> args_;     // index l = 1..L (0 unused)
@@ -287,6 +293,7 @@ class PlanT final : public Plan {
   std::vector<T*> D_;                  // compact coefficient arrays 1..L-1 (decompose)
   std::vector<T*> Z_;                  // corrections 1..L
   T* stage_[2] = {nullptr, nullptr};
+  T* W_ = nullptr;                     // scratch of the windowed (out-of-place) Thomas passes
   char* tables_ = nullptr;
   char* ws_ = nullptr;
   std::size_t ws_bytes_ = 0;
@@ -297,6 +304,7 @@ class PlanT final : public Plan {
 template <class T>
 PlanT<T>::PlanT(const Hierarchy& hier) {
   h = hier;
+  if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   HGR_CUDA_CHECK(cudaGetDevice(&device));
   const int rank = h.rank, Lv = h.L;
@@ -411,6 +419,14 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
     off_z[std::size_t(l)] = total;
     total += (nelem(l - 1) * esz + 255) & ~std::size_t(255);
   }
+  std::size_t w_n = 0;
+  for (int l = 1; l <= Lv; ++l) {
+    for (int k = 3 - rank; k < 3; ++k)
+      if (thomas_needs_out_of_place<T>(ext_[std::size_t(l) - 1].data(), k))
+        w_n = std::max(w_n, nelem(l - 1));
+  }
+  const std::size_t off_w = total;
+  total += (w_n * esz + 255) & ~std::size_t(255);
   const std::size_t off_s0 = total;
   total += (stage_n[0] * esz + 255) & ~std::size_t(255);
   const std::size_t off_s1 = total;
@@ -423,6 +439,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   D_.assign(std::size_t(Lv) + 1, nullptr);
   for (int l = 1; l < Lv; ++l) D_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_d[std::size_t(l)]);
   for (int l = 1; l <= Lv; ++l) Z_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_z[std::size_t(l)]);
+  if (w_n) W_ = reinterpret_cast<T*>(ws_ + off_w);
   stage_[0] = reinterpret_cast<T*>(ws_ + off_s0);
   stage_[1] = reinterpret_cast<T*>(ws_ + off_s1);
   HGR_CUDA_CHECK(cudaMalloc(&d_flag_, sizeof(int)));
@@ -458,33 +475,75 @@ void PlanT<T>::correction(int l, const T* in, T* z, T* apply, int sign, cudaStre
     e[k] = a.c[k];
     cur = dst;
   }
+  // Thomas passes: register-tiled kernels where the line fits them (windowed
+  // passes ping-pong between z and W_), else one thread per line
+  T* zc = z;
+  const int64_t n = e[0] * e[1] * e[2];
+  bool applied = false;
   for (int k = 3 - rank; k < 3; ++k) {
     const bool last = k == 2;
-    prof_begin(kKindThomas, sz() * 2.0 * double(e[0] * e[1] * e[2]), s);
-    launch_thomas<T>(z, e, k, a.mult[k], a.rpiv[k], a.upper[k], last ? apply : nullptr, sign, s);
+    prof_begin(kKindThomas, sz() * 2.0 * double(n), s);
+    T* dst = thomas_needs_out_of_place<T>(e, k) ? (zc == W_ ? z : W_) : zc;
+    if (launch_thomas_fast<T>(zc, dst, e, k, a.mult[k], a.rpiv[k], a.upper[k], s)) {
+      zc = dst;
+    } else {
+      launch_thomas<T>(zc, e, k, a.mult[k], a.rpiv[k], a.upper[k], last ? apply : nullptr, sign, s);
+      applied = last && apply;
+    }
     prof_end(s);
     ++launch_count_;
   }
+  if (apply && !applied) {
+    launch_axpy<T>(apply, zc, n, sign, s);
+    ++launch_count_;
+  } else if (!apply && zc != z) {
+    HGR_CUDA_CHECK(cudaMemcpyAsync(z, zc, std::size_t(n) * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  }
 }
 
-// Thomas passes (thomas_pass, correction.hpp:335-339) on z over the real dims
-// in ascending order; the last pass writes last_out (which may equal z).
+// Thomas passes (thomas_pass, correction.hpp:335-339) over the real dims in
+// ascending order, starting from `src` (the load vector, clobbered); the last
+// pass writes last_out. Passes that cut lines into overlapping windows run out
+// of place between z and the scratch W_, the others in place.
 template <class T>
-void PlanT<T>::thomas_all(int l, T* z, T* last_out, cudaStream_t s) {
+bool PlanT<T>::thomas_route(int l, const T* src, const T* last_out) const {
   const LevelArgs<T>& a = args_[std::size_t(l)];
   const int64_t c[3] = {a.c[0], a.c[1], a.c[2]};
+  const T* cur = src;
   for (int k = 3 - h.rank; k < 3; ++k) {
-    T* dst = (k == 2) ? last_out : z;
+    const bool win = thomas_needs_out_of_place<T>(c, k);
+    if (k == 2) return !(win && cur == last_out);
+    if (win) cur = cur == W_ ? Z_[std::size_t(l)] : W_;
+  }
+  return true;
+}
+
+template <class T>
+T* PlanT<T>::thomas_src(int l, T* last_out) const {
+  T* z = Z_[std::size_t(l)];
+  return thomas_route(l, z, last_out) ? z : W_;
+}
+
+template <class T>
+void PlanT<T>::thomas_all(int l, T* src, T* last_out, cudaStream_t s) {
+  const LevelArgs<T>& a = args_[std::size_t(l)];
+  const int64_t c[3] = {a.c[0], a.c[1], a.c[2]};
+  T* cur = src;
+  for (int k = 3 - h.rank; k < 3; ++k) {
+    T* dst = cur;
+    if (k == 2) dst = last_out;
+    else if (thomas_needs_out_of_place<T>(c, k)) dst = cur == W_ ? Z_[std::size_t(l)] : W_;
     ++launch_count_;
     prof_begin(kKindThomas, sz() * 2.0 * double(c[0] * c[1] * c[2]), s);
-    const bool fast = launch_thomas_fast<T>(z, dst, c, k, a.mult[k], a.rpiv[k], a.upper[k], s);
+    const bool fast = launch_thomas_fast<T>(cur, dst, c, k, a.mult[k], a.rpiv[k], a.upper[k], s);
     if (!fast) {
-      launch_thomas<T>(z, c, k, a.mult[k], a.rpiv[k], a.upper[k], nullptr, 0, s);
-      if (dst != z)
-        HGR_CUDA_CHECK(cudaMemcpyAsync(dst, z, std::size_t(c[0] * c[1] * c[2]) * sizeof(T),
+      launch_thomas<T>(cur, c, k, a.mult[k], a.rpiv[k], a.upper[k], nullptr, 0, s);
+      if (dst != cur)
+        HGR_CUDA_CHECK(cudaMemcpyAsync(dst, cur, std::size_t(c[0] * c[1] * c[2]) * sizeof(T),
                                        cudaMemcpyDeviceToDevice, s));
     }
     prof_end(s);
+    cur = dst;
   }
 }
 
@@ -642,13 +701,14 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     const double n = double(h.node_count(l)), c = double(h.node_count(l - 1));
     if (big(l)) {
       // read the level once, write the load vector and the gathered coarse nodes
+      T* zl = thomas_src(l, Z_[std::size_t(l)]);
       prof_begin(kKindFusedRec, sz() * (n + 2 * c), s);
-      const bool ok = launch_level_fused<T>(src, nullptr, Z_[std::size_t(l)],
-                                            C_[std::size_t(l) - 1], a, kFusedRecompose, nullptr, s);
+      const bool ok = launch_level_fused<T>(src, nullptr, zl, C_[std::size_t(l) - 1], a,
+                                            kFusedRecompose, nullptr, s);
       prof_end(s);
       if (ok) {
         ++launch_count_;
-        thomas_all(l, Z_[std::size_t(l)], Z_[std::size_t(l)], s);
+        thomas_all(l, zl, Z_[std::size_t(l)], s);
         continue;
       }
     }
