@@ -39,18 +39,21 @@ namespace {
 //   With a window start ws the tables cover line positions ws .. ws+NP-1
 //   (positions outside the line are padding).
 template <class T>
-__device__ void build_tables(T* tm, T* tP, T* tp, T* tu, T* tQ, int n, int NC, int CH,
+__device__ void build_tables(T* tm, T* tP, T* tp, T* tu, T* tQ, int n, int NC, int CH, int CHP,
                              const T* mult, const T* rpiv, const T* upper, int ws = 0) {
-  const int NP = NC * CH;
-  for (int i = threadIdx.x; i < NP; i += blockDim.x) {
-    const int pos = ws + i;
-    tm[i] = (pos >= 1 && pos < n) ? mult[pos - 1] : T(0);
-    tp[i] = (pos >= 0 && pos < n) ? rpiv[pos] : T(0);
-    tu[i] = (pos >= 0 && pos < n - 1) ? upper[pos] : T(0);
+  // chunk q's entries live at q*CHP .. q*CHP+CH-1 (CHP: CH rounded up to a
+  // 16-byte multiple, so a chunk's table is read with vector loads); pad = 0
+  for (int i = threadIdx.x; i < NC * CHP; i += blockDim.x) {
+    const int q = i / CHP, k = i - q * CHP;
+    const int pos = ws + q * CH + k;
+    const bool in = k < CH;
+    tm[i] = (in && pos >= 1 && pos < n) ? mult[pos - 1] : T(0);
+    tp[i] = (in && pos >= 0 && pos < n) ? rpiv[pos] : T(0);
+    tu[i] = (in && pos >= 0 && pos < n - 1) ? upper[pos] : T(0);
   }
   __syncthreads();
   for (int q = threadIdx.x; q < NC; q += blockDim.x) {
-    const int s = q * CH;
+    const int s = q * CHP;
     T a = T(1);
     for (int k = 0; k < CH; ++k) {
       a *= -tm[s + k];
@@ -61,9 +64,116 @@ __device__ void build_tables(T* tm, T* tP, T* tp, T* tu, T* tQ, int n, int NC, i
       b *= -(tu[s + k] * tp[s + k]);
       tQ[s + k] = b;
     }
+    for (int k = CH; k < CHP; ++k) tP[s + k] = tQ[s + k] = T(0);
   }
   __syncthreads();
 }
+
+// table stride of a chunk of CH positions: CH rounded up to 16 bytes
+template <class T, int CH>
+constexpr int chunk_pitch() {
+  return (CH + int(16 / sizeof(T)) - 1) / int(16 / sizeof(T)) * int(16 / sizeof(T));
+}
+
+// 16-byte vector of T
+template <class T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void split(const float4& v, float (&o)[4]) {
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int N = 2;
+  static __device__ __forceinline__ void split(const double2& v, double (&o)[2]) {
+    o[0] = v.x; o[1] = v.y;
+  }
+};
+
+// Chunk solves reading the (16-byte aligned, chunk-pitched) tables with vector
+// loads: one shared-memory load per 16 bytes of table instead of per entry.
+template <class T, int CH, int LPT = 1>
+struct ChunkSolveV {
+  using V = Vec16<T>;
+  static constexpr int N = V::N;
+  static __device__ __forceinline__ void fwd_local(T (&x)[LPT][CH], const T* tm, T (&g)[LPT]) {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) g[u] = T(0);
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += N) {
+      T m[N];
+      V::split(reinterpret_cast<const typename V::type*>(tm)[k0 / N], m);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if (k0 + j < CH) {
+#pragma unroll
+          for (int u = 0; u < LPT; ++u) {
+            g[u] = x[u][k0 + j] - m[j] * g[u];
+            x[u][k0 + j] = g[u];
+          }
+        }
+      }
+    }
+  }
+  static __device__ __forceinline__ void apply(T (&x)[LPT][CH], const T* tab, const T (&c)[LPT]) {
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += N) {
+      T t[N];
+      V::split(reinterpret_cast<const typename V::type*>(tab)[k0 / N], t);
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+        if (k0 + j < CH) {
+#pragma unroll
+          for (int u = 0; u < LPT; ++u) x[u][k0 + j] += t[j] * c[u];
+        }
+    }
+  }
+  static __device__ __forceinline__ void bwd_local(T (&x)[LPT][CH], const T* tu, const T* tp,
+                                                   T (&h)[LPT]) {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) h[u] = T(0);
+    constexpr int K0 = (CH - 1) / N * N;
+#pragma unroll
+    for (int k0 = K0; k0 >= 0; k0 -= N) {
+      T uu[N], pp[N];
+      V::split(reinterpret_cast<const typename V::type*>(tu)[k0 / N], uu);
+      V::split(reinterpret_cast<const typename V::type*>(tp)[k0 / N], pp);
+#pragma unroll
+      for (int j = N - 1; j >= 0; --j) {
+        if (k0 + j < CH) {
+#pragma unroll
+          for (int u = 0; u < LPT; ++u) {
+            h[u] = (x[u][k0 + j] - uu[j] * h[u]) * pp[j];
+            x[u][k0 + j] = h[u];
+          }
+        }
+      }
+    }
+  }
+  // single-line forms
+  static __device__ __forceinline__ T fwd_local(T (&x)[CH], const T* tm) {
+    T (&xx)[1][CH] = *reinterpret_cast<T(*)[1][CH]>(&x);
+    T g[1];
+    ChunkSolveV<T, CH, 1>::fwd_local(xx, tm, g);
+    return g[0];
+  }
+  static __device__ __forceinline__ void apply(T (&x)[CH], const T* tab, T c) {
+    T (&xx)[1][CH] = *reinterpret_cast<T(*)[1][CH]>(&x);
+    const T cc[1] = {c};
+    ChunkSolveV<T, CH, 1>::apply(xx, tab, cc);
+  }
+  static __device__ __forceinline__ T bwd_local(T (&x)[CH], const T* tu, const T* tp) {
+    T (&xx)[1][CH] = *reinterpret_cast<T(*)[1][CH]>(&x);
+    T h[1];
+    ChunkSolveV<T, CH, 1>::bwd_local(xx, tu, tp, h);
+    return h[0];
+  }
+};
 
 // chunk solves of LPT lines at once (the line-independent table values are
 // loaded once for all of them)
@@ -164,20 +274,21 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     k_thomas_lines(const T* in, T* out, int n, int sd, int so, int na, int c2, int nfull,
                    int ntail, int nlg, int S, int J, const T* __restrict__ mult,
                    const T* __restrict__ rpiv, const T* __restrict__ upper) {
-  constexpr int NT = 32 * kLW, NC = kLW, NP = NC * CH, GW = 32 * LPT;
+  constexpr int NT = 32 * kLW, NC = kLW, GW = 32 * LPT;
+  constexpr int CHP = chunk_pitch<T, CH>(), NTB = NC * CHP;
   constexpr int H = window_halo<T>();
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
-  T* tP = tm + NP;
-  T* tp = tP + NP;
-  T* tu = tp + NP;
-  T* tQ = tu + NP;
-  T* sf = tQ + NP;         // [NC][GW] forward chunk summaries
+  T* tP = tm + NTB;
+  T* tp = tP + NTB;
+  T* tu = tp + NTB;
+  T* tQ = tu + NTB;
+  T* sf = tQ + NTB;        // [NC][GW] forward chunk summaries
   T* sb = sf + NC * GW;    // [NC][GW] backward chunk summaries
   T* land = sb + NC * GW;  // [CH][NT][LPT] per-thread landing zone
-  if (!WIN) build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
+  if (!WIN) build_tables(tm, tP, tp, tu, tQ, n, NC, CH, CHP, mult, rpiv, upper);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int s0 = w * CH;
+  const int s0 = w * CH, ts = w * CHP;  // chunk start position, table offset
   const int kmax = n - s0 < CH ? n - s0 : CH;  // valid positions of this warp's chunk (!WIN)
   const int nfull_groups = na * nfull;
   const int ngroups = WIN ? nlg * J : nlg;
@@ -214,6 +325,15 @@ __global__ void __launch_bounds__(32 * kLW, 1)
           ptx::cp_async_elem<int(sizeof(T))>(ld + k * NT * LPT + u, in + (ok ? off + p * sd : 0),
                                              ok ? int(sizeof(T)) : 0);
         }
+      }
+    } else if (g < nfull_groups && kmax == CH) {
+      const int off = line_off(g, 0);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+#pragma unroll
+        for (int u = 0; u < LPT; ++u)
+          ptx::cp_async_elem<int(sizeof(T))>(ld + k * NT * LPT + u, in + (off + k * sd + u),
+                                             int(sizeof(T)));
       }
     } else if (g < nfull_groups) {
       const T* src = in + line_off(g, 0);
@@ -254,11 +374,16 @@ __global__ void __launch_bounds__(32 * kLW, 1)
       }
     } else {
       const int off = line_off(g, 0);
-      const T* src = in + (off < 0 ? 0 : off);
+      if (off >= 0 && kmax == CH) {  // full chunk: no per-element predicates
 #pragma unroll
-      for (int k = 0; k < CH; ++k) {
-        nx[k] = (off >= 0 && k < kmax) ? __ldg(src) : T(0);
-        if (k + 1 < kmax) src += sd;
+        for (int k = 0; k < CH; ++k) nx[k] = __ldg(in + (off + k * sd));
+      } else {
+        const T* src = in + (off < 0 ? 0 : off);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+          nx[k] = (off >= 0 && k < kmax) ? __ldg(src) : T(0);
+          if (k + 1 < kmax) src += sd;
+        }
       }
     }
   };
@@ -274,7 +399,7 @@ __global__ void __launch_bounds__(32 * kLW, 1)
       if (wi != cur_w) {  // every thread is past the previous group's table reads
         cur_w = wi;
         __syncthreads();
-        build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper, wstart(g));
+        build_tables(tm, tP, tp, tu, tQ, n, NC, CH, CHP, mult, rpiv, upper, wstart(g));
       }
     }
     T x[LPT][CH];
@@ -300,31 +425,31 @@ __global__ void __launch_bounds__(32 * kLW, 1)
 
     // forward: local solve, exact carry scan over the chunks before this one
     T e[LPT], c[LPT];
-    ChunkSolve<T, CH, LPT>::fwd_local(x, tm + s0, e);
+    ChunkSolveV<T, CH, LPT>::fwd_local(x, tm + ts, e);
 #pragma unroll
     for (int u = 0; u < LPT; ++u) sf[w * GW + LPT * lane + u] = e[u];
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < LPT; ++u) c[u] = T(0);
     for (int v = w > scan_depth<T, CH>() ? w - scan_depth<T, CH>() : 0; v < w; ++v) {
-      const T pe = tP[v * CH + CH - 1];
+      const T pe = tP[v * CHP + CH - 1];
 #pragma unroll
       for (int u = 0; u < LPT; ++u) c[u] = sf[v * GW + LPT * lane + u] + pe * c[u];
     }
-    ChunkSolve<T, CH, LPT>::apply(x, tP + s0, c);
+    ChunkSolveV<T, CH, LPT>::apply(x, tP + ts, c);
     // backward: local solve, carry scan over the chunks after this one
-    ChunkSolve<T, CH, LPT>::bwd_local(x, tu + s0, tp + s0, e);
+    ChunkSolveV<T, CH, LPT>::bwd_local(x, tu + ts, tp + ts, e);
 #pragma unroll
     for (int u = 0; u < LPT; ++u) sb[w * GW + LPT * lane + u] = e[u];
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < LPT; ++u) c[u] = T(0);
     for (int v = w + scan_depth<T, CH>() < NC - 1 ? w + scan_depth<T, CH>() : NC - 1; v > w; --v) {
-      const T qs = tQ[v * CH];
+      const T qs = tQ[v * CHP];
 #pragma unroll
       for (int u = 0; u < LPT; ++u) c[u] = sb[v * GW + LPT * lane + u] + qs * c[u];
     }
-    ChunkSolve<T, CH, LPT>::apply(x, tQ + s0, c);
+    ChunkSolveV<T, CH, LPT>::apply(x, tQ + ts, c);
 
     if constexpr (WIN) {
       const int wi = g / nlg, ws = wstart(g), p0 = ws + s0;
@@ -338,6 +463,13 @@ __global__ void __launch_bounds__(32 * kLW, 1)
           const int p = p0 + k;
           if (p >= lo && p < hi) out[off + p * sd] = x[u][k];
         }
+      }
+    } else if (g < nfull_groups && kmax == CH) {
+      const int off = line_off(g, 0);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+#pragma unroll
+        for (int u = 0; u < LPT; ++u) out[off + k * sd + u] = x[u][k];
       }
     } else if (g < nfull_groups) {
       T* dst = out + line_off(g, 0);
@@ -373,14 +505,16 @@ struct RowsCfg {
   static constexpr int CPW = 32 / R;         // chunks per warp
   static constexpr int NC = NW * CPW;        // chunks per row
   static constexpr int NP = NC * CH;
+  static constexpr int CHP = chunk_pitch<T, CH>(), NTB = NC * CHP;  // table entries
+  // byte offset of the first tile (16-byte aligned)
+  static constexpr size_t tiles_off = (size_t(5) * NTB + size_t(2) * NC * R) * sizeof(T) / 16 * 16 + 16;
   // a tile holds R rows of n; the last row's padded chunk positions read up to NP past its start
   static __host__ __device__ size_t buf_elems(int n) {
     return (size_t(R - 1) * n + (NP > n ? NP : n) + 15) / 16 * 16;
   }
   // two input tiles (loads double-buffered) and, with STAGE, one output staging tile
   static size_t smem(int n) {
-    return (size_t(5) * NP + size_t(2) * NC * R + (STAGE ? 3 : 2) * buf_elems(n)) * sizeof(T) +
-           16 + 2 * 8;
+    return tiles_off + (STAGE ? 3 : 2) * buf_elems(n) * sizeof(T) + 2 * 8;
   }
 };
 
@@ -392,27 +526,26 @@ __global__ void __launch_bounds__(512, 1)
     k_thomas_rows(const T* in, T* out, int64_t rows, int n, const T* __restrict__ mult,
                   const T* __restrict__ rpiv, const T* __restrict__ upper) {
   using C = RowsCfg<T, CH, R, STAGE>;
-  constexpr int NC = C::NC, NP = C::NP, CPW = C::CPW;
+  constexpr int NC = C::NC, CPW = C::CPW, CHP = C::CHP, NTB = C::NTB;
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
-  T* tP = tm + NP;
-  T* tp = tP + NP;
-  T* tu = tp + NP;
-  T* tQ = tu + NP;
-  T* sf = tQ + NP;       // [NC][R]
+  T* tP = tm + NTB;
+  T* tp = tP + NTB;
+  T* tu = tp + NTB;
+  T* tQ = tu + NTB;
+  T* sf = tQ + NTB;      // [NC][R]
   T* sb = sf + NC * R;   // [NC][R]
   const size_t BE = C::buf_elems(n);
-  T* buf0 = reinterpret_cast<T*>(
-      (reinterpret_cast<uintptr_t>(sb + NC * R) + 15) & ~uintptr_t(15));
+  T* buf0 = reinterpret_cast<T*>(smem_t + C::tiles_off);
   T* ot = buf0 + 2 * BE;  // output staging tile (STAGE)
   uint64_t* bar = reinterpret_cast<uint64_t*>(buf0 + (STAGE ? 3 : 2) * BE);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int r = lane % R, q = w * CPW + lane / R, s0 = q * CH;
+  const int r = lane % R, q = w * CPW + lane / R, s0 = q * CH, ts = q * CHP;
   const int64_t ngroups = (rows + R - 1) / R;
 
   // zero the tiles once: positions past a row's end then read finite data
   for (size_t i = tid; i < (STAGE ? 3 : 2) * BE; i += blockDim.x) buf0[i] = T(0);
-  build_tables(tm, tP, tp, tu, tQ, n, NC, CH, mult, rpiv, upper);
+  build_tables(tm, tP, tp, tu, tQ, n, NC, CH, CHP, mult, rpiv, upper);
   if (tid == 0) {
     ptx::mbar_init(&bar[0], 1);
     ptx::mbar_init(&bar[1], 1);
@@ -444,21 +577,21 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int k = 0; k < CH; ++k) x[k] = mine[k];
 
-    sf[q * R + r] = ChunkSolve<T, CH>::fwd_local(x, tm + s0);
+    sf[q * R + r] = ChunkSolveV<T, CH>::fwd_local(x, tm + ts);
     __syncthreads();
     // every thread has read its chunk: the input tile takes group g + 2G
     if (STAGE && tid == 0 && g + 2 * G < ngroups) load(g + 2 * G, b);
     T c = T(0);
     for (int v = q > scan_depth<T, CH>() ? q - scan_depth<T, CH>() : 0; v < q; ++v)
-      c = sf[v * R + r] + tP[v * CH + CH - 1] * c;
-    ChunkSolve<T, CH>::apply(x, tP + s0, c);
-    sb[q * R + r] = ChunkSolve<T, CH>::bwd_local(x, tu + s0, tp + s0);
+      c = sf[v * R + r] + tP[v * CHP + CH - 1] * c;
+    ChunkSolveV<T, CH>::apply(x, tP + ts, c);
+    sb[q * R + r] = ChunkSolveV<T, CH>::bwd_local(x, tu + ts, tp + ts);
     if (STAGE && tid == 0) ptx::bulk_wait_read0();  // the previous store has read `ot`
     __syncthreads();
     c = T(0);
     for (int v = q + scan_depth<T, CH>() < NC - 1 ? q + scan_depth<T, CH>() : NC - 1; v > q; --v)
-      c = sb[v * R + r] + tQ[v * CH] * c;
-    ChunkSolve<T, CH>::apply(x, tQ + s0, c);
+      c = sb[v * R + r] + tQ[v * CHP] * c;
+    ChunkSolveV<T, CH>::apply(x, tQ + ts, c);
 
     T* dst = (STAGE ? ot : buf0 + b * BE) + r * n + s0;
 #pragma unroll
@@ -642,8 +775,9 @@ void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, 
   constexpr int LPT = 1;
   constexpr bool RP = sizeof(T) == 4;
   constexpr int NT = 32 * kLW, NP = kLW * CH, GW = 32 * LPT;
+  constexpr int NTB = kLW * chunk_pitch<T, CH>();
   const size_t smem =
-      (size_t(5) * NP + 2 * kLW * GW + (RP ? 0 : size_t(CH) * NT * LPT)) * sizeof(T);
+      (size_t(5) * NTB + 2 * kLW * GW + (RP ? 0 : size_t(CH) * NT * LPT)) * sizeof(T);
   auto kern = k_thomas_lines<T, CH, LPT, RP, WIN>;
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int n = int(e[dim]);
