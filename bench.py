@@ -285,6 +285,16 @@ def run_gpu(args, cfg):
     nbytes = x.numel() * S
     stream = torch.cuda.current_stream(dev)
 
+    # tile-segment autotuning, outside every timed region
+    tune_info = None
+    if not args.no_autotune:
+        t0 = time.perf_counter()
+        rep = plan.autotune(x, P)
+        torch.cuda.synchronize(dev)
+        ents = rep["kernels"]
+        tune_info = {"seconds": round(time.perf_counter() - t0, 3), "kernels_tuned": len(ents),
+                     "changed": sum(1 for e in ents if e["chosen_s0"] != e["heuristic_s0"])}
+
     def step():
         plan.decompose_into(x, P)
         plan.recompose_into(P, x, L)
@@ -398,6 +408,7 @@ def run_gpu(args, cfg):
                 "path": "pinned host field -> device, hgr Plan decompose+recompose, "
                         "max |error| scalar -> host"},
         "gpu_launches": launches_step * args.steps,
+        "autotune": tune_info,
         "clocks": clocks,
         "roundtrip_rel_err": rt_err,
         "checksum": chk_sum,
@@ -421,6 +432,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="budget of the cpu_baseline sample (rank 0, N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-autotune", action="store_true",
+                    help="keep the built-in segment heuristics (skip Plan.autotune)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

@@ -96,6 +96,22 @@ int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream);
 int hgr_cuda_plan_set_profiling(hgr_plan plan, int enable);
 int hgr_cuda_plan_read_profile(hgr_plan plan, double* ms, double* bytes, long* launches);
 
+/* Tile-segment autotuning (the reference ranks launch
+ * configurations with its sector model, perf_model.hpp:71-137 rank_configs /
+ * top_k, and leaves the measuring to its caller). For every level on the
+ * fused kernels the segment lengths of the decompose, recompose and
+ * interpolation kernels are ranked by the same kind of model and the top three
+ * are timed on this device; the fastest is kept by the plan. d_in is read,
+ * d_out and the workspace are overwritten. Synchronizes `stream`. The JSON
+ * report (per level and kernel: candidates with model and measured times, the
+ * heuristic's and the chosen segment) is copied to `report` (truncated to
+ * report_bytes - 1 characters; may be NULL); *report_len (may be NULL) gets its
+ * full length. */
+int hgr_cuda_plan_autotune(hgr_plan plan, const void* d_in, void* d_out, void* stream,
+                           char* report, size_t report_bytes, size_t* report_len);
+/* back to the built-in segment heuristics */
+int hgr_cuda_plan_reset_tuning(hgr_plan plan);
+
 /* Synthetic input (bench/test data): u = a[i]*b[j] + c[k] +
  * 1e-3*eta(seed + flat) with eta from splitmix64 in [-1, 1), computed in
  * double with IEEE-exact mul/add and rounded once to the dtype. The factor

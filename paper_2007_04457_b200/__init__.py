@@ -26,6 +26,7 @@ device memory and streams only; all arithmetic runs in the CUDA library.
 from __future__ import annotations
 
 import ctypes as C
+import json
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -204,7 +205,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _lib.load().hgr_cuda_plan_destroy(h)
+            try:
+                _lib.load().hgr_cuda_plan_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     @property
@@ -234,6 +238,24 @@ class Plan:
 
     def sync_status(self, stream: Optional[int] = None) -> None:
         _check(_lib.load().hgr_cuda_plan_sync_status(self._h, stream))
+
+    def autotune(self, src, out, stream: Optional[int] = None) -> dict:
+        """Tile-segment autotuning: rank the segment lengths of the
+        fused decompose / recompose / interpolation kernels per level with the
+        sector model (perf_model.hpp:71-137), time the top three, keep the
+        fastest. src is read, out is overwritten. Returns the JSON report."""
+        lib = _lib.load()
+        st = stream if stream is not None else _stream_of(src)
+        n = C.c_size_t(0)
+        buf = C.create_string_buffer(1 << 20)  # ~100 bytes per candidate
+        _check(lib.hgr_cuda_plan_autotune(self._h, _ptr(src), _ptr(out), st, buf, len(buf),
+                                          C.byref(n)))
+        if n.value >= len(buf):
+            raise HgrError("autotune report truncated")
+        return json.loads(buf.value.decode())
+
+    def reset_tuning(self) -> None:
+        _check(_lib.load().hgr_cuda_plan_reset_tuning(self._h))
 
     KINDS = ("fused_decompose_level", "fused_recompose_level", "thomas", "recompose_interp",
              "assembly", "small_levels")

@@ -47,6 +47,8 @@ _SIGS = {
     "hgr_cuda_plan_sync_status": (_int, [_vp, _vp]),
     "hgr_cuda_plan_set_profiling": (_int, [_vp, _int]),
     "hgr_cuda_plan_read_profile": (_int, [_vp, _vp, _vp, _vp]),
+    "hgr_cuda_plan_autotune": (_int, [_vp, _vp, _vp, _vp, C.c_char_p, _sz, C.POINTER(_sz)]),
+    "hgr_cuda_plan_reset_tuning": (_int, [_vp]),
     "hgr_cuda_synthetic_field_f64": (_int, [_G, _vp, C.c_ulonglong, _vp, _vp, _vp, _vp]),
     "hgr_cuda_synthetic_field_f32": (_int, [_G, _vp, C.c_ulonglong, _vp, _vp, _vp, _vp]),
     "hgr_class_node_count": (_sz, [_G, _int]),

@@ -1,5 +1,6 @@
 // capi.cu -- extern "C" boundary (include/hgr_cuda.h). Every entry point maps
 // hgrb::Error (and CUDA failures) to an hgr_status + thread-local message.
+#include <algorithm>
 #include <cstring>
 #include <list>
 #include <memory>
@@ -371,6 +372,28 @@ int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream) {
     if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
   });
   return rc;
+}
+
+int hgr_cuda_plan_autotune(hgr_plan plan, const void* d_in, void* d_out, void* stream,
+                           char* report, size_t report_bytes, size_t* report_len) {
+  return guarded([&] {
+    hgrb::require(plan != nullptr, "plan is null");
+    hgrb::require(d_in != nullptr && d_out != nullptr, "autotune: null operand");
+    const std::string rep = plan->plan->autotune(d_in, d_out, as_stream(stream));
+    if (report_len) *report_len = rep.size();
+    if (report && report_bytes) {
+      const size_t n = std::min(rep.size(), report_bytes - 1);
+      std::memcpy(report, rep.data(), n);
+      report[n] = 0;
+    }
+  });
+}
+
+int hgr_cuda_plan_reset_tuning(hgr_plan plan) {
+  return guarded([&] {
+    hgrb::require(plan != nullptr, "plan is null");
+    plan->plan->reset_tuning();
+  });
 }
 
 int hgr_cuda_plan_set_profiling(hgr_plan plan, int enable) {

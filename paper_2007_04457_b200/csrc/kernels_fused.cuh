@@ -1,6 +1,8 @@
 // kernels_fused.cuh -- launchers of the bandwidth-optimised sm_100a kernels.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace hgrb {
@@ -32,15 +34,37 @@ enum FusedMode : int {
 // memory through cp.async.bulk (TMA bulk-copy engine) into an mbarrier ring.
 // Returns false if the level is not supported (caller falls back).
 // flag (decompose mode, may be null): set to 1 if any input value is NaN/Inf.
+// s0: coarse planes per CTA segment along dim 0 (0 = built-in heuristic).
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
-                        int mode, int* flag, cudaStream_t s);
+                        int mode, int* flag, cudaStream_t s, int s0 = 0);
 
 // Recompose interpolation (GPK^-1, refactor.hpp:77-87): coarse = C - Z (Z may be
 // null), out[coarse] = coarse, out[refined] = (with ? coef : 0) + interp(coarse).
 // 3D tiles with the coarse block staged in shared memory. in-place safe.
 template <class T>
 bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
-                       bool with_coeffs, cudaStream_t s);
+                       bool with_coeffs, cudaStream_t s, int s0 = 0);
+
+// Tile-segment candidates of the level / interpolation kernels ranked by a
+// sector-traffic model (the reference's perf_model.hpp:71-100 estimate_time
+// restated for these tiles: every row a CTA moves padded to 32-byte sectors,
+// reads + writes, times the blocks covering the level, over the bandwidth,
+// times the wave-quantisation loss of 148 SMs x resident CTAs). Sorted by
+// model time, ties in candidate order. s0 = 0 marks the heuristic's choice.
+struct SegChoice {
+  int s0;           // coarse planes per CTA segment
+  int blocks;       // CTAs launched
+  double model_us;  // model time
+};
+template <class T>
+std::vector<SegChoice> level_fused_candidates(const LevelArgs<T>& a, int mode, double bw_gbs);
+template <class T>
+std::vector<SegChoice> interp_candidates(const LevelArgs<T>& a, bool with_coeffs, bool has_z,
+                                         double bw_gbs);
+template <class T>
+int level_fused_default_s0(const LevelArgs<T>& a);
+template <class T>
+int interp_default_s0(const LevelArgs<T>& a);
 
 }  // namespace hgrb

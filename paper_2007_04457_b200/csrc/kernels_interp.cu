@@ -16,6 +16,7 @@
 // safe (every cell is read before it is written, by the CTA that owns it).
 // The last fine row and column of the level are the faces of k_interp_face.
 #include <algorithm>
+#include <cmath>
 
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
@@ -320,7 +321,8 @@ __global__ void __launch_bounds__(256)
   };
   const int n = face == 0 ? e1 : e2 - 1;
   const int64_t pbase = int64_t(j) * e1 * e2;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+  const int q1 = min(n, int(blockIdx.z + 1) * int(blockDim.x));
+  for (int q = int(blockIdx.z * blockDim.x + threadIdx.x); q < q1; q += blockDim.x) {
     const int r = face == 0 ? q : e1 - 1, c = face == 0 ? e2 - 1 : q;
     const int64_t idx = pbase + int64_t(r) * e2 + c;
     if (((j | r | c) & 1) == 0) {
@@ -332,9 +334,25 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+template <class T>
+int interp_tiles(const LevelArgs<T>& a) {
+  using Cf = ICfg<T>;
+  const int64_t nt1 = (a.c[1] - 1 + Cf::TW1 - 1) / Cf::TW1;
+  const int64_t nt2 = (a.c[2] - 1 + Cf::TW2 - 1) / Cf::TW2;
+  return int(nt1 * nt2);
+}
+
+template <class T>
+int interp_heuristic_s0(const LevelArgs<T>& a) {
+  const int64_t tiles = interp_tiles(a);
+  int S0 = kMaxSegI;
+  while (S0 > 4 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
+  return S0;
+}
+
 template <class T, bool WITH, bool HASZ>
 void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs<T>& a,
-                cudaStream_t s) {
+                cudaStream_t s, int s0) {
   using Cf = ICfg<T>;
   auto kern = k_interp_march<T, WITH, HASZ>;
   static int attr_dev = -1;
@@ -348,8 +366,7 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
   const int nt1 = int((a.c[1] - 1 + Cf::TW1 - 1) / Cf::TW1);
   const int nt2 = int((a.c[2] - 1 + Cf::TW2 - 1) / Cf::TW2);
   const int64_t tiles = int64_t(nt1) * nt2;
-  int S0 = kMaxSegI;
-  while (S0 > 4 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
+  const int S0 = s0 > 0 ? std::min(s0, kMaxSegI) : interp_heuristic_s0(a);
   const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
   constexpr int V = Cf::V;
   const int64_t plane_f = a.e[1] * a.e[2], plane_c = a.c[1] * a.c[2];
@@ -383,23 +400,64 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
 
 template <class T>
 bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
-                       bool with, cudaStream_t s) {
+                       bool with, cudaStream_t s, int s0) {
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (a.e[1] < 3 || a.e[2] < 3 || !al(C) || (Z && !al(Z)) || (with && !al(coef))) return false;
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
   if (a.c[0] * a.c[1] * a.c[2] >= (int64_t(1) << 31)) return false;
-  if (with && Z) run_interp<T, true, true>(coef, out, C, Z, a, s);
-  else if (with) run_interp<T, true, false>(coef, out, C, Z, a, s);
-  else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s);
-  else run_interp<T, false, false>(coef, out, C, Z, a, s);
-  k_interp_face<T><<<dim3(unsigned(a.e[0]), 2), 256, 0, s>>>(coef, out, C, Z, a, with);
+  if (with && Z) run_interp<T, true, true>(coef, out, C, Z, a, s, s0);
+  else if (with) run_interp<T, true, false>(coef, out, C, Z, a, s, s0);
+  else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s, s0);
+  else run_interp<T, false, false>(coef, out, C, Z, a, s, s0);
+  k_interp_face<T><<<dim3(unsigned(a.e[0]), 2, unsigned((std::max(a.e[1], a.e[2]) + 255) / 256)),
+                     256, 0, s>>>(coef, out, C, Z, a, with);
   HGR_CUDA_CHECK(cudaGetLastError());
   return true;
 }
 
+template <class T>
+int interp_default_s0(const LevelArgs<T>& a) {
+  return interp_heuristic_s0(a);
+}
+
+template <class T>
+std::vector<SegChoice> interp_candidates(const LevelArgs<T>& a, bool with, bool hasz,
+                                         double bw_gbs) {
+  using Cf = ICfg<T>;
+  const double S = double(sizeof(T));
+  const int64_t tiles = interp_tiles(a);
+  const double slots = 148.0 * Cf::MINB;
+  auto sectors = [&](double elems) { return std::ceil(elems * S / 32.0) * 32.0 / S; };
+  std::vector<SegChoice> out;
+  int last_nseg = -1;
+  for (int S0 = kMaxSegI; S0 >= 1; S0 /= 2) {
+    const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
+    if (nseg == last_nseg) continue;
+    last_nseg = nseg;
+    const double fine = std::min<double>(double(a.e[0]), 2.0 * S0 + 1);
+    const double coarse = std::min<double>(double(a.c[0]), S0 + 1.0);
+    double elems = fine * Cf::FR * sectors(Cf::FC);                       // output rows
+    if (with) elems += fine * Cf::FR * sectors(Cf::BOX);                  // coefficient rows
+    elems += (hasz ? 2 : 1) * coarse * Cf::CR * sectors(Cf::CBOX);        // coarse (+ Z) rows
+    const double blocks = double(tiles) * nseg;
+    const double waves = std::ceil(blocks / slots) / (blocks / slots);
+    out.push_back({S0, int(blocks), blocks * elems * S / (bw_gbs * 1e3) * waves});
+  }
+  std::stable_sort(out.begin(), out.end(),
+                   [](const SegChoice& x, const SegChoice& y) { return x.model_us < y.model_us; });
+  return out;
+}
+
+template int interp_default_s0<float>(const LevelArgs<float>&);
+template int interp_default_s0<double>(const LevelArgs<double>&);
+template std::vector<SegChoice> interp_candidates<float>(const LevelArgs<float>&, bool, bool,
+                                                         double);
+template std::vector<SegChoice> interp_candidates<double>(const LevelArgs<double>&, bool, bool,
+                                                          double);
+
 template bool launch_interp_rec<float>(const float*, float*, const float*, const float*,
-                                       const LevelArgs<float>&, bool, cudaStream_t);
+                                       const LevelArgs<float>&, bool, cudaStream_t, int);
 template bool launch_interp_rec<double>(const double*, double*, const double*, const double*,
-                                        const LevelArgs<double>&, bool, cudaStream_t);
+                                        const LevelArgs<double>&, bool, cudaStream_t, int);
 
 }  // namespace hgrb

@@ -40,6 +40,7 @@
 //   them) are the faces of k_level_face, so every tile is a full TW1 x 64 block
 //   or a clipped one.
 #include <algorithm>
+#include <cmath>
 
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
@@ -500,7 +501,9 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
 // first reduces the 3 fine columns (rows) next to the face with K2 (K1) for the
 // 5 fine planes of its coarse plane into shared memory, then every thread forms
 // its output from 25 of those sums.
-constexpr int kFaceSeg = 256;  // coarse outputs of faces 0/1 per CTA (2x fine for faces 2/3)
+// Face CTAs are small (latency-bound strided reads): faces 0/1 take kFaceSeg
+// coarse outputs per CTA, faces 2/3 kFaceCells fine cells (one per thread).
+constexpr int kFaceSeg = 64, kFaceCells = 256;
 
 template <class T, int MODE>
 __global__ void __launch_bounds__(256)
@@ -524,6 +527,7 @@ __global__ void __launch_bounds__(256)
     const int q1 = min(nout, q0 + kFaceSeg);
     const int f_lo = max(0, 2 * q0 - 2), W = min(ne, 2 * q1 + 1) - f_lo;
     // R[a][f] = sum over the 3 fine cells next to the face (K2 or K1 boundary row)
+#pragma unroll 3
     for (int idx = tid; idx < 5 * W; idx += nt) {
       const int x = idx / W, f = f_lo + idx - x * W;
       const int f0 = 2 * i0 - 2 + x;
@@ -573,9 +577,9 @@ __global__ void __launch_bounds__(256)
     return U[(2 * b0) * plane + (2 * b1) * e2 + 2 * b2];
   };
   const int n = face == 2 ? e1 : e2 - 1;
-  const int q0 = int(blockIdx.z) * 2 * kFaceSeg;
+  const int q0 = int(blockIdx.z) * kFaceCells;
   if (q0 >= n) return;
-  const int q1 = min(n, q0 + 2 * kFaceSeg);
+  const int q1 = min(n, q0 + kFaceCells);
   bool bad = false;
   for (int q = q0 + tid; q < q1; q += nt) {
     const int r = face == 2 ? q : e1 - 1, c = face == 2 ? e2 - 1 : q;
@@ -601,9 +605,25 @@ void set_level_face_smem(size_t bytes) {
   }
 }
 
+template <class T>
+int fused_tiles(const LevelArgs<T>& a) {
+  using C = LCfg<T>;
+  const int64_t nt1 = (a.c[1] - 1 + C::TW1 - 1) / C::TW1;
+  const int64_t nt2 = (a.c[2] - 1 + C::TW2 - 1) / C::TW2;
+  return int(nt1 * nt2);
+}
+
+template <class T>
+int fused_heuristic_s0(const LevelArgs<T>& a) {
+  const int64_t tiles = fused_tiles(a);
+  int S0 = kMaxSeg;
+  while (S0 > 8 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
+  return S0;
+}
+
 template <class T, int MODE>
 void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int* flag,
-               cudaStream_t s) {
+               cudaStream_t s, int s0) {
   using C = LCfg<T>;
   auto kern = k_level_fused<T, MODE>;
   static int attr_dev = -1;
@@ -617,8 +637,7 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
   const int nt1 = int((a.c[1] - 1 + C::TW1 - 1) / C::TW1);
   const int nt2 = int((a.c[2] - 1 + C::TW2 - 1) / C::TW2);
   const int64_t tiles = int64_t(nt1) * nt2;
-  int S0 = kMaxSeg;
-  while (S0 > 8 && tiles * std::max<int64_t>(1, (a.c[0] - 1) / S0) < 1200) S0 /= 2;
+  const int S0 = s0 > 0 ? std::min(s0, kMaxSeg) : fused_heuristic_s0(a);
   const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
   // 1D TMA coordinates are 32-bit: split the segments into launches whose planes
   // fit below 2^31 elements from the launch's own (16-byte aligned) map base.
@@ -643,7 +662,9 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
     HGR_CUDA_CHECK(cudaGetLastError());
     sa = sb;
   }
-  const int64_t fseg = (std::max(a.e[1], a.e[2]) + 2 * kFaceSeg - 1) / (2 * kFaceSeg) + 1;
+  const int64_t fseg =
+      std::max((std::max(a.c[1], a.c[2]) + kFaceSeg - 1) / kFaceSeg,
+               MODE == kFusedDecompose ? (std::max(a.e[1], a.e[2]) + kFaceCells - 1) / kFaceCells : 0);
   const dim3 fgrid(unsigned(std::max(a.c[0], a.e[0])), MODE == kFusedDecompose ? 4 : 2,
                    unsigned(fseg));
   const size_t fsmem = size_t(5) * size_t(2 * kFaceSeg + 3) * sizeof(T);
@@ -656,23 +677,62 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
 
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
-                        int mode, int* flag, cudaStream_t s) {
+                        int mode, int* flag, cudaStream_t s, int s0) {
   // TMA needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
   if ((reinterpret_cast<uintptr_t>(U) & 15) != 0) return false;
   if (a.e[1] < 3 || a.e[2] < 3 || a.h[2] == nullptr) return false;  // 1D: reference path
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
   if (mode == kFusedDecompose)
-    run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, a, flag, s);
+    run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, a, flag, s, s0);
   else if (mode == kFusedLoadOnly)
-    run_fused<T, kFusedLoadOnly>(U, coef_out, zload, gather, a, flag, s);
+    run_fused<T, kFusedLoadOnly>(U, coef_out, zload, gather, a, flag, s, s0);
   else
-    run_fused<T, kFusedRecompose>(U, coef_out, zload, gather, a, flag, s);
+    run_fused<T, kFusedRecompose>(U, coef_out, zload, gather, a, flag, s, s0);
   return true;
 }
 
+template <class T>
+int level_fused_default_s0(const LevelArgs<T>& a) {
+  return fused_heuristic_s0(a);
+}
+
+template <class T>
+std::vector<SegChoice> level_fused_candidates(const LevelArgs<T>& a, int mode, double bw_gbs) {
+  using C = LCfg<T>;
+  const double S = double(sizeof(T));
+  const int64_t tiles = fused_tiles(a);
+  const double slots = 148.0 * C::MINB;
+  auto sectors = [&](double elems) { return std::ceil(elems * S / 32.0) * 32.0 / S; };
+  std::vector<SegChoice> out;
+  int last_nseg = -1;
+  for (int S0 = kMaxSeg; S0 >= 1; S0 /= 2) {
+    const int nseg = int(std::max<int64_t>(1, (a.c[0] - 1) / S0));
+    if (nseg == last_nseg) continue;
+    last_nseg = nseg;
+    const double planes = std::min<double>(double(a.e[0]), 2.0 * S0 + 3);   // fine planes read
+    const double outp = std::min<double>(double(a.e[0]), 2.0 * S0);         // fine planes owned
+    double elems = planes * C::RW * sectors(C::BOX);                         // TMA rows read
+    if (mode == kFusedDecompose) elems += outp * 2 * C::TW1 * sectors(2 * C::TW2);  // coefficients
+    elems += std::min<double>(double(a.c[0]), S0) * C::TW1 * sectors(C::TW2);       // load vector
+    if (mode == kFusedRecompose) elems += std::min<double>(double(a.c[0]), S0) * C::TW1 * sectors(C::TW2);
+    const double blocks = double(tiles) * nseg;
+    const double waves = std::ceil(blocks / slots) / (blocks / slots);
+    out.push_back({S0, int(blocks), blocks * elems * S / (bw_gbs * 1e3) * waves});
+  }
+  std::stable_sort(out.begin(), out.end(),
+                   [](const SegChoice& x, const SegChoice& y) { return x.model_us < y.model_us; });
+  return out;
+}
+
+template int level_fused_default_s0<float>(const LevelArgs<float>&);
+template int level_fused_default_s0<double>(const LevelArgs<double>&);
+template std::vector<SegChoice> level_fused_candidates<float>(const LevelArgs<float>&, int, double);
+template std::vector<SegChoice> level_fused_candidates<double>(const LevelArgs<double>&, int,
+                                                                double);
+
 template bool launch_level_fused<float>(const float*, float*, float*, float*,
-                                        const LevelArgs<float>&, int, int*, cudaStream_t);
+                                        const LevelArgs<float>&, int, int*, cudaStream_t, int);
 template bool launch_level_fused<double>(const double*, double*, double*, double*,
-                                         const LevelArgs<double>&, int, int*, cudaStream_t);
+                                         const LevelArgs<double>&, int, int*, cudaStream_t, int);
 
 }  // namespace hgrb

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -129,6 +130,12 @@ void Plan::read_profile(KindStats out[kKindCount]) {
   }
   prof_pending_.clear();
   for (int i = 0; i < kKindCount; ++i) out[i] = prof_acc_[i];
+}
+
+void Plan::clear_graphs() {
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  graphs_.clear();
 }
 
 void Plan::run_graphed(int dir, const void* in, const void* out, int m, cudaStream_t s,
@@ -263,6 +270,8 @@ class PlanT final : public Plan {
   void decompose(void* d_data, cudaStream_t s) override;
   void recompose(const void* d_in, void* d_out, int upto, cudaStream_t s) override;
   int launches(int direction, int upto) override;
+  std::string autotune(const void* d_in, void* d_out, cudaStream_t s) override;
+  void reset_tuning() override;
   std::size_t workspace_bytes() const override { return ws_bytes_; }
   void interpolate_to_fine(int level, const void* coarse, void* fine, cudaStream_t s) override;
   void compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) override;
@@ -294,6 +303,8 @@ class PlanT final : public Plan {
   std::vector<T*> Z_;                  // corrections 1..L
   T* stage_[2] = {nullptr, nullptr};
   T* W_ = nullptr;                     // scratch of the windowed (out-of-place) Thomas passes
+  // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
+  std::vector<int> s0_dec_, s0_rec_, s0_int_;
   char* tables_ = nullptr;
   char* ws_ = nullptr;
   std::size_t ws_bytes_ = 0;
@@ -306,6 +317,9 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   h = hier;
   if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
+  s0_dec_.assign(std::size_t(h.L) + 1, 0);
+  s0_rec_.assign(std::size_t(h.L) + 1, 0);
+  s0_int_.assign(std::size_t(h.L) + 1, 0);
   HGR_CUDA_CHECK(cudaGetDevice(&device));
   const int rank = h.rank, Lv = h.L;
   ext_.resize(std::size_t(Lv) + 1);
@@ -561,7 +575,7 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
       // read the level once, write the coefficients and the load vector once
       prof_begin(kKindFusedDec, sz() * (n + (n - c) + c), s);
       const bool ok = launch_level_fused<T>(src, coef_dst, z, nullptr, a, kFusedDecompose,
-                                            top ? d_flag_ : nullptr, s);
+                                            top ? d_flag_ : nullptr, s, s0_dec_[std::size_t(l)]);
       prof_end(s);
       if (ok) {
         ++launch_count_;
@@ -570,7 +584,8 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
       }
     } else {
       prof_begin(kKindFusedDec, sz() * (n + c), s);
-      const bool ok = launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s);
+      const bool ok = launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s,
+                                            s0_dec_[std::size_t(l)]);
       prof_end(s);
       if (ok) {
         prof_begin(kKindSmall, sz() * (n + (n - c)), s);
@@ -704,7 +719,7 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
       T* zl = thomas_src(l, Z_[std::size_t(l)]);
       prof_begin(kKindFusedRec, sz() * (n + 2 * c), s);
       const bool ok = launch_level_fused<T>(src, nullptr, zl, C_[std::size_t(l) - 1], a,
-                                            kFusedRecompose, nullptr, s);
+                                            kFusedRecompose, nullptr, s, s0_rec_[std::size_t(l)]);
       prof_end(s);
       if (ok) {
         ++launch_count_;
@@ -731,7 +746,7 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     if (big(l)) {
       prof_begin(kKindInterp, bytes, s);
       const bool ok = launch_interp_rec<T>(coef, dst, C_[std::size_t(l) - 1], Z,
-                                           args_[std::size_t(l)], with, s);
+                                           args_[std::size_t(l)], with, s, s0_int_[std::size_t(l)]);
       prof_end(s);
       if (ok) continue;
     }
@@ -772,6 +787,92 @@ void PlanT<T>::compute_correction(int level, const void* coeffs, void* z, cudaSt
   require(*h_flag_ == 0,
           "compute_correction: coefficients must be zero at coarse-grid positions");
   correction(level, static_cast<const T*>(coeffs), static_cast<T*>(z), nullptr, 0, s);
+}
+
+template <class T>
+void PlanT<T>::reset_tuning() {
+  std::fill(s0_dec_.begin(), s0_dec_.end(), 0);
+  std::fill(s0_rec_.begin(), s0_rec_.end(), 0);
+  std::fill(s0_int_.begin(), s0_int_.end(), 0);
+  clear_graphs();
+}
+
+template <class T>
+std::string PlanT<T>::autotune(const void* d_in, void* d_out, cudaStream_t s) {
+  require(!profiling_, "autotune: disable profiling first");
+  const int Lv = L();
+  const T* in = static_cast<const T*>(d_in);
+  T* out = static_cast<T*>(d_out);
+  double bw = 6540.0;  // GB/s; only the ranking depends on it
+  if (const char* v = std::getenv("HGR_MODEL_HBM_GBS")) bw = std::atof(v);
+  cudaEvent_t e0, e1;
+  HGR_CUDA_CHECK(cudaEventCreate(&e0));
+  HGR_CUDA_CHECK(cudaEventCreate(&e1));
+  // time one launch sequence: one warm run, then the mean of two
+  auto time_us = [&](const std::function<void()>& run) {
+    run();
+    HGR_CUDA_CHECK(cudaEventRecord(e0, s));
+    run();
+    run();
+    HGR_CUDA_CHECK(cudaEventRecord(e1, s));
+    HGR_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    HGR_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    return 1e3 * double(ms) / 2.0;
+  };
+  std::string rep = "{\"hbm_model_gbs\": " + std::to_string(bw) + ", \"kernels\": [";
+  bool first = true;
+  auto tune = [&](int l, const char* name, std::vector<SegChoice> cands, int dflt,
+                  const std::function<void(int)>& run, int& slot) {
+    const std::size_t k = std::min<std::size_t>(3, cands.size());
+    double best = 0;
+    int best_s0 = 0;
+    std::string cj;
+    for (std::size_t i = 0; i < cands.size(); ++i) {
+      double us = -1;
+      if (i < k) {
+        us = time_us([&] { run(cands[i].s0); });
+        if (best_s0 == 0 || us < best) best = us, best_s0 = cands[i].s0;
+      }
+      cj += std::string(i ? ", " : "") + "{\"s0\": " + std::to_string(cands[i].s0) +
+            ", \"blocks\": " + std::to_string(cands[i].blocks) +
+            ", \"model_us\": " + std::to_string(cands[i].model_us) +
+            ", \"measured_us\": " + (us < 0 ? std::string("null") : std::to_string(us)) + "}";
+    }
+    slot = best_s0;
+    rep += std::string(first ? "" : ", ") + "{\"level\": " + std::to_string(l) +
+           ", \"kernel\": \"" + name + "\", \"heuristic_s0\": " + std::to_string(dflt) +
+           ", \"chosen_s0\": " + std::to_string(best_s0) + ", \"candidates\": [" + cj + "]}";
+    first = false;
+  };
+  for (int l = Lv; l >= 1; --l) {
+    if (!big(l) || h.rank < 3) continue;  // rank < 3: one plane, nothing to segment
+    const LevelArgs<T>& a = args_[std::size_t(l)];
+    const T* src = l == Lv ? in : C_[std::size_t(l)];
+    T* coef = l == Lv ? out : D_[std::size_t(l)];
+    T* z = Z_[std::size_t(l)];
+    T* gat = C_[std::size_t(l) - 1];
+    // operands the fused kernels accept (16-byte aligned); else the level is not fused
+    if (!launch_level_fused<T>(src, coef, z, nullptr, a, kFusedDecompose, nullptr, s)) continue;
+    tune(l, "decompose_level", level_fused_candidates<T>(a, kFusedDecompose, bw),
+         level_fused_default_s0<T>(a),
+         [&](int v) { launch_level_fused<T>(src, coef, z, nullptr, a, kFusedDecompose, nullptr, s, v); },
+         s0_dec_[std::size_t(l)]);
+    tune(l, "recompose_level", level_fused_candidates<T>(a, kFusedRecompose, bw),
+         level_fused_default_s0<T>(a),
+         [&](int v) { launch_level_fused<T>(src, nullptr, z, gat, a, kFusedRecompose, nullptr, s, v); },
+         s0_rec_[std::size_t(l)]);
+    T* dst = l == Lv ? out : C_[std::size_t(l)];
+    const T* cf = l == Lv ? in : C_[std::size_t(l)];
+    tune(l, "recompose_interp", interp_candidates<T>(a, true, true, bw), interp_default_s0<T>(a),
+         [&](int v) { launch_interp_rec<T>(cf, dst, gat, z, a, true, s, v); },
+         s0_int_[std::size_t(l)]);
+  }
+  rep += "]}";
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  clear_graphs();
+  return rep;
 }
 
 template <class T>

@@ -88,6 +88,16 @@ class Plan {
   virtual void compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) = 0;
   virtual void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) = 0;
 
+  // Tile-segment autotuning (perf_model.hpp:71-137): for every
+  // level on the fused kernels, rank the segment lengths of the decompose,
+  // recompose and interpolation kernels with the sector model, time the top
+  // three on this device with d_in / d_out / the workspace as operands (d_out
+  // and the workspace are overwritten) and keep the fastest. Returns a JSON
+  // report; later calls replay with the tuned launches (graphs are rebuilt).
+  virtual std::string autotune(const void* d_in, void* d_out, cudaStream_t s) = 0;
+  // drop the tuning (back to the built-in heuristics)
+  virtual void reset_tuning() = 0;
+
  protected:
   int* d_flag_ = nullptr;   // non-finite flag set by the level-L decompose kernel
   int* h_flag_ = nullptr;   // pinned mirror
@@ -122,6 +132,7 @@ class Plan {
     unsigned long last_use;
   };
   std::vector<GraphEntry> graphs_;
+  void clear_graphs();
   unsigned long graph_clock_ = 0;
   cudaStream_t gstream_ = nullptr;
   cudaEvent_t gev_[2] = {nullptr, nullptr};
