@@ -23,6 +23,24 @@ bool launch_thomas_fast(const T* in, T* out, const int64_t ext[3], int dim, cons
 template <class T>
 bool thomas_needs_out_of_place(const int64_t ext[3], int dim);
 
+// The coarse tail (kernels_tail.cu): levels 1..lt of a plan in one CTA per
+// direction. Per level: its arguments and compact buffers.
+template <class T>
+struct TailLevel {
+  LevelArgs<T> a;
+  T* src;     // compact level-l array C_l (decompose input; recompose coefficients, in place)
+  T* coef;    // D_l: decompose coefficients
+  T* coarse;  // C_{l-1}
+  T* z;       // Z_l
+};
+template <class T>
+void launch_tail_decompose(const TailLevel<T>* d_levels, int lt, int rank, T* s0, T* s1,
+                           cudaStream_t s);
+// prefix m: levels <= m use their stored coefficients
+template <class T>
+void launch_tail_recompose(const TailLevel<T>* d_levels, int lt, int m, int rank, T* s0, T* s1,
+                           cudaStream_t s);
+
 enum FusedMode : int {
   kFusedDecompose = 0,  // coefficients -> coef_out, K*U -> zload
   kFusedLoadOnly = 1,   // K*U -> zload only

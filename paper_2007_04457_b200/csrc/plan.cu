@@ -288,6 +288,13 @@ class PlanT final : public Plan {
   bool thomas_route(int l, const T* src, const T* last_out) const;
   T* thomas_src(int l, T* last_out) const;
   void assemble(T* out, cudaStream_t s);
+  void tail_decompose(cudaStream_t s) {
+    if (tail_lt_ <= 0) return;
+    prof_begin(kKindSmall, 0.0, s);
+    launch_tail_decompose<T>(tail_dev_, tail_lt_, h.rank, stage_[0], stage_[1], s);
+    prof_end(s);
+    ++launch_count_;
+  }
   static constexpr double sz() { return double(sizeof(T)); }
   void decompose_level(int l, const T* src, T* coef_dst, bool in_place, cudaStream_t s);
   // levels with at least big_nodes_ nodes run the fused / TMA kernels, smaller
@@ -303,6 +310,10 @@ class PlanT final : public Plan {
   std::vector<T*> Z_;                  // corrections 1..L
   T* stage_[2] = {nullptr, nullptr};
   T* W_ = nullptr;                     // scratch of the windowed (out-of-place) Thomas passes
+  // coarse tail: levels 1..tail_lt_ (all below the fused threshold, under the
+  // top) run as one single-CTA launch per direction (kernels_tail.cu)
+  int tail_lt_ = 0;
+  TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
   std::vector<int> s0_dec_, s0_rec_, s0_int_;
   char* tables_ = nullptr;
@@ -455,7 +466,25 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   for (int l = 1; l <= Lv; ++l) Z_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_z[std::size_t(l)]);
   if (w_n) W_ = reinterpret_cast<T*>(ws_ + off_w);
   stage_[0] = reinterpret_cast<T*>(ws_ + off_s0);
+  {
+    // one CTA is the better engine only while a level is a few thousand nodes
+    // (tuning knob HGR_TAIL_NODES, 0 disables the tail)
+    std::size_t tail_nodes = 1200;
+    if (const char* v = std::getenv("HGR_TAIL_NODES")) tail_nodes = std::size_t(std::atoll(v));
+    for (int l = Lv - 1; l >= 1; --l)
+      if (!big(l) && h.node_count(l) <= tail_nodes) { tail_lt_ = l; break; }
+  }
   stage_[1] = reinterpret_cast<T*>(ws_ + off_s1);
+  if (tail_lt_ > 0) {
+    std::vector<TailLevel<T>> tl(std::size_t(tail_lt_) + 1);
+    for (int l = 1; l <= tail_lt_; ++l)
+      tl[std::size_t(l)] = TailLevel<T>{args_[std::size_t(l)], C_[std::size_t(l)],
+                                        D_[std::size_t(l)], C_[std::size_t(l) - 1],
+                                        Z_[std::size_t(l)]};
+    HGR_CUDA_CHECK(cudaMalloc(&tail_dev_, tl.size() * sizeof(TailLevel<T>)));
+    HGR_CUDA_CHECK(cudaMemcpy(tail_dev_, tl.data(), tl.size() * sizeof(TailLevel<T>),
+                              cudaMemcpyHostToDevice));
+  }
   HGR_CUDA_CHECK(cudaMalloc(&d_flag_, sizeof(int)));
   HGR_CUDA_CHECK(cudaMemset(d_flag_, 0, sizeof(int)));
   HGR_CUDA_CHECK(cudaMallocHost(&h_flag_, sizeof(int)));
@@ -465,6 +494,7 @@ template <class T>
 PlanT<T>::~PlanT() {
   cudaFree(tables_);
   cudaFree(ws_);
+  cudaFree(tail_dev_);
   cudaFree(d_flag_);
   cudaFreeHost(h_flag_);
 }
@@ -654,8 +684,9 @@ void PlanT<T>::decompose_to_direct(const void* d_in, void* d_out, cudaStream_t s
     last_launches_[0] = launch_count_;
     return;
   }
-  for (int l = Lv; l >= 1; --l)
+  for (int l = Lv; l > tail_lt_; --l)
     decompose_level(l, l == Lv ? in : C_[std::size_t(l)], l == Lv ? out : D_[std::size_t(l)], false, s);
+  tail_decompose(s);
   assemble(out, s);
   last_launches_[0] = launch_count_;
 }
@@ -673,7 +704,9 @@ void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
     return;
   }
   decompose_level(Lv, data, data, true, s);
-  for (int l = Lv - 1; l >= 1; --l) decompose_level(l, C_[std::size_t(l)], D_[std::size_t(l)], false, s);
+  for (int l = Lv - 1; l > tail_lt_; --l)
+    decompose_level(l, C_[std::size_t(l)], D_[std::size_t(l)], false, s);
+  tail_decompose(s);
   assemble(data, s);
   last_launches_[0] = launch_count_;
 }
@@ -710,7 +743,7 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     prof_end(s);
     ++launch_count_;
   }
-  for (int l = m; l >= 1; --l) {
+  for (int l = m; l > tail_lt_; --l) {
     const T* src = l == Lv ? in : C_[std::size_t(l)];
     const LevelArgs<T>& a = args_[std::size_t(l)];
     const double n = double(h.node_count(l)), c = double(h.node_count(l - 1));
@@ -734,7 +767,13 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     prof_end(s);
     ++launch_count_;
   }
-  for (int l = 1; l <= Lv; ++l) {
+  if (tail_lt_ > 0) {
+    prof_begin(kKindSmall, 0.0, s);
+    launch_tail_recompose<T>(tail_dev_, tail_lt_, m, h.rank, stage_[0], stage_[1], s);
+    prof_end(s);
+    ++launch_count_;
+  }
+  for (int l = tail_lt_ + 1; l <= Lv; ++l) {
     const bool with = l <= m;
     const T* coef = l == Lv ? in : C_[std::size_t(l)];
     T* dst = l == Lv ? out : C_[std::size_t(l)];
