@@ -64,6 +64,15 @@ template <class T>
 bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
                        bool with_coeffs, cudaStream_t s, int s0 = 0);
 
+// 1D grids (canonical (1, 1, n)): the fused level / interpolation steps as
+// per-coarse-node streams (kernels_line.cu). Return false if not 1D.
+template <class T>
+bool launch_line_level(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int mode,
+                       int* flag, cudaStream_t s);
+template <class T>
+bool launch_line_interp(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
+                        bool with_coeffs, cudaStream_t s);
+
 // Tile-segment candidates of the level / interpolation kernels ranked by a
 // sector-traffic model (the reference's perf_model.hpp:71-100 estimate_time
 // restated for these tiles: every row a CTA moves padded to 32-byte sectors,

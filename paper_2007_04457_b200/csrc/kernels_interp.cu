@@ -401,6 +401,7 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
 template <class T>
 bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
                        bool with, cudaStream_t s, int s0) {
+  if (a.e[0] == 1 && a.e[1] == 1) return launch_line_interp<T>(coef, out, C, Z, a, with, s);
   const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (a.e[1] < 3 || a.e[2] < 3 || !al(C) || (Z && !al(Z)) || (with && !al(coef))) return false;
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;

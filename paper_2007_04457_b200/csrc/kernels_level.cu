@@ -679,8 +679,9 @@ template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
                         int mode, int* flag, cudaStream_t s, int s0) {
   // TMA needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
+  if (a.e[0] == 1 && a.e[1] == 1) return launch_line_level<T>(U, coef_out, zload, gather, a, mode, flag, s);
   if ((reinterpret_cast<uintptr_t>(U) & 15) != 0) return false;
-  if (a.e[1] < 3 || a.e[2] < 3 || a.h[2] == nullptr) return false;  // 1D: reference path
+  if (a.e[1] < 3 || a.e[2] < 3 || a.h[2] == nullptr) return false;
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
   if (mode == kFusedDecompose)
     run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, a, flag, s, s0);

@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(512, 1)
     const T* mine = buf0 + b * BE + r * n + s0;
     T x[CH];
 #pragma unroll
-    for (int k = 0; k < CH; ++k) x[k] = mine[k];
+    for (int k = 0; k < CH; ++k) x[k] = s0 + k < n ? mine[k] : T(0);  // padding: 0, whatever the tile holds
 
     sf[q * R + r] = ChunkSolveV<T, CH>::fwd_local(x, tm + ts);
     __syncthreads();

@@ -458,6 +458,9 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   total += (stage_n[1] * esz + 255) & ~std::size_t(255);
   ws_bytes_ = total;
   if (total) HGR_CUDA_CHECK(cudaMalloc(&ws_, total));
+  // debug / test knob: NaN-fill the workspace so a read-before-write shows up
+  if (const char* v = std::getenv("HGR_POISON_WORKSPACE"))
+    if (total && v[0] == '1') HGR_CUDA_CHECK(cudaMemset(ws_, 0xFF, total));
   C_.resize(std::size_t(Lv));
   Z_.assign(std::size_t(Lv) + 1, nullptr);
   for (int l = 0; l < Lv; ++l) C_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_c[std::size_t(l)]);
