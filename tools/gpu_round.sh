@@ -7,12 +7,14 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>
 timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err
-for c in 1025f64 513f32 aniso_nu_f64 513sq_f64; do
+for c in 1025f64 513f32 aniso_nu_f64 513sq_f64 8193sq_f32 line_f64; do
   timeout 300 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/ncu_launches_1025f64.csv python tools/prof_one.py 1025x1025x1025 f64 > $O/ncu.log 2>&1
+python tools/ncu_summary.py $O/ncu_launches_1025f64.csv 1 200 > $O/ncu_launches_1025f64.summary.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/ncu_launches_1025f32.csv python tools/prof_one.py 1025x1025x1025 f32 >> $O/ncu.log 2>&1
+python tools/ncu_summary.py $O/ncu_launches_1025f32.csv 1 200 > $O/ncu_launches_1025f32.summary.txt 2>&1
 echo done
 # ncu --set full of the dominant kernel (top-level decompose level kernel), both precisions
 timeout 600 bash tools/ncu_one.sh $TAG/full_dec_f64 "k_level_fused.*0>" 6 1025x1025x1025 f64 >> $O/ncu.log 2>&1

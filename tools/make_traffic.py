@@ -22,9 +22,13 @@ def per_trip(path):
         d = agg.setdefault(i, {'name': name})
         d[r['Metric Name']] = float(r['Metric Value'].replace(',', ''))
     ids = sorted(agg)
-    # the second (warm) round trip starts at the second decompose's first fused launch
-    dec = [i for i in ids if re.search(r"k_level_fused<\w+, 0>", agg[i]['name'])]
-    start = dec[len(dec) // 2]
+    # the measured round trip follows the last marker (fill) kernel of tools/prof_one.py
+    marks = [i for i in ids if re.search(r"[Ff]ill", agg[i]['name'])]
+    if marks:
+        start = marks[-1] + 1
+    else:  # older lists: the second decompose's first fused launch
+        dec = [i for i in ids if re.search(r"k_level_fused<\w+, 0>", agg[i]['name'])]
+        start = dec[len(dec) // 2]
     return [agg[i] for i in ids if i >= start]
 
 out_path = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"

@@ -1,4 +1,5 @@
-"""Summarise an ncu --csv launch list: per-launch time and DRAM bytes (second half = steady state)."""
+"""Summarise an ncu --csv launch list: per-launch time and DRAM bytes of the measured round
+trip (after the last marker fill kernel of tools/prof_one.py; else the second half)."""
 import csv, collections, sys, io
 path = sys.argv[1]
 frac = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
@@ -6,6 +7,9 @@ lines = [l for l in open(path) if l.startswith('"')]
 rows = list(csv.DictReader(io.StringIO(''.join(lines))))
 ids = sorted({int(r['ID']) for r in rows})
 start = ids[int(len(ids) * (1 - frac))] if frac < 1 else 0
+marks = sorted({int(r['ID']) for r in rows if 'ill' in r['Kernel Name'] and 'Fill' in r['Kernel Name'] or 'fill' in r['Kernel Name']})
+if marks:  # tools/prof_one.py: the measured round trip follows the last marker fill kernel
+    start = marks[-1] + 1
 agg = collections.OrderedDict()
 for r in rows:
     i = int(r['ID'])
