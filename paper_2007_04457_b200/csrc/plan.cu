@@ -288,9 +288,29 @@ class PlanT final : public Plan {
   bool thomas_route(int l, const T* src, const T* last_out) const;
   T* thomas_src(int l, T* last_out) const;
   void assemble(T* out, cudaStream_t s);
+  // SURVEY §8(d) reference-step bytes of levels 1..lt (one direction)
+  double tail_model_bytes() const {
+    double total = 0;
+    for (int l = 1; l <= tail_lt_; ++l) {
+      const auto& e = ext_[std::size_t(l)];
+      const auto& c = ext_[std::size_t(l) - 1];
+      const int D = h.rank, k0 = 3 - D;
+      const double n = double(e[0] * e[1] * e[2]), cn = double(c[0] * c[1] * c[2]), r = n - cn;
+      std::vector<double> st(std::size_t(D) + 1);
+      for (int k = 0; k <= D; ++k) {  // s_k: the first k real dims coarse
+        double v = 1;
+        for (int d = 0; d < D; ++d) v *= double(d < k ? c[std::size_t(k0 + d)] : e[std::size_t(k0 + d)]);
+        st[std::size_t(k)] = v;
+      }
+      double b = (n + r) + (r + st[1]);
+      for (int k = 1; k < D; ++k) b += st[std::size_t(k)] + st[std::size_t(k) + 1];
+      total += sz() * (b + 2.0 * D * cn + 3.0 * cn);
+    }
+    return total;
+  }
   void tail_decompose(cudaStream_t s) {
     if (tail_lt_ <= 0) return;
-    prof_begin(kKindSmall, 0.0, s);
+    prof_begin(kKindSmall, tail_model_bytes(), s);
     launch_tail_decompose<T>(tail_dev_, tail_lt_, h.rank, stage_[0], stage_[1], s);
     prof_end(s);
     ++launch_count_;
@@ -771,7 +791,7 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     ++launch_count_;
   }
   if (tail_lt_ > 0) {
-    prof_begin(kKindSmall, 0.0, s);
+    prof_begin(kKindSmall, tail_model_bytes(), s);
     launch_tail_recompose<T>(tail_dev_, tail_lt_, m, h.rank, stage_[0], stage_[1], s);
     prof_end(s);
     ++launch_count_;
