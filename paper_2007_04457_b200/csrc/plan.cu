@@ -462,7 +462,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   }
   for (int l = 1; l <= Lv; ++l) {
     off_z[std::size_t(l)] = total;
-    total += (nelem(l - 1) * esz + 255) & ~std::size_t(255);
+    total += (nelem(l - 1) * esz + 511) & ~std::size_t(255);
   }
   std::size_t w_n = 0;
   for (int l = 1; l <= Lv; ++l) {
@@ -471,11 +471,11 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
         w_n = std::max(w_n, nelem(l - 1));
   }
   const std::size_t off_w = total;
-  total += (w_n * esz + 255) & ~std::size_t(255);
+  total += (w_n * esz + 511) & ~std::size_t(255);
   const std::size_t off_s0 = total;
-  total += (stage_n[0] * esz + 255) & ~std::size_t(255);
+  total += (stage_n[0] * esz + 511) & ~std::size_t(255);
   const std::size_t off_s1 = total;
-  total += (stage_n[1] * esz + 255) & ~std::size_t(255);
+  total += (stage_n[1] * esz + 511) & ~std::size_t(255);
   ws_bytes_ = total;
   if (total) HGR_CUDA_CHECK(cudaMalloc(&ws_, total));
   // debug / test knob: NaN-fill the workspace so a read-before-write shows up
