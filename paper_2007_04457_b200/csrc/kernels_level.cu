@@ -40,6 +40,7 @@
 //   them) are the faces of k_level_face, so every tile is a full TW1 x 64 block
 //   or a clipped one.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -124,6 +125,30 @@ __device__ __forceinline__ void load7f(const float* row, int base, float (&v)[7]
 #pragma unroll
   for (int k = 0; k < 7; ++k) v[k] = w[k + PH];
 }
+// fp64 with a compile-time parity of pos = base + PH (base even)
+template <class T, int PH>
+__device__ __forceinline__ void load5c(const T* row, int base, T (&v)[5]) {
+  using T2 = typename Vec2<T>::type;
+  const int pos = base + PH;
+  if constexpr (PH == 0) {
+    const T2 x = *reinterpret_cast<const T2*>(row + pos);
+    const T2 y = *reinterpret_cast<const T2*>(row + pos + 2);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; v[4] = row[pos + 4];
+  } else {
+    const T2 x = *reinterpret_cast<const T2*>(row + pos + 1);
+    const T2 y = *reinterpret_cast<const T2*>(row + pos + 3);
+    v[0] = row[pos]; v[1] = x.x; v[2] = x.y; v[3] = y.x; v[4] = y.y;
+  }
+}
+// loadV with the row phase known at compile time (no per-row dispatch)
+template <class T, int NV, int PH>
+__device__ __forceinline__ void loadVc(const T* row, int base, T (&v)[NV]) {
+  if constexpr (NV == 5) load5c<T, PH>(row, base, v);
+  else load7f<PH>(row, base, v);
+}
+template <int N>
+using IC = std::integral_constant<int, N>;
+
 // the lane's window values: NV = 2*CPL+3 values starting at window column base
 template <class T, int NV>
 __device__ __forceinline__ void loadV(const T* row, int ph, int base, T (&v)[NV]) {
@@ -282,6 +307,8 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   for (int p = 0; p < nplanes && p < NS; ++p) issue(j0 + p);
 
   const int e2m = int(e2 & (V - 1));
+  // rows and planes advance the phase by one (every 2^k+1 extent with k >= 2)
+  const bool ph_regular = e2m == 1 && (plane_sz & (V - 1)) == 1;
   const int ph00 = int((wr0 * e2 + wc0) & (V - 1));
   // phase (shared-memory position of window column 0) of row r in a plane of phase phj
   auto plane_ph = [&](int64_t jj) { return int((jj * plane_sz + ph00) & (V - 1)); };
@@ -396,13 +423,15 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
     }
     if (has_band) {
       if (jodd || !DEC) {
-        // K path only (odd planes; recompose / load-only modes)
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
+        // K path only (odd planes; recompose / load-only modes); PH: the row's
+        // phase, or -1 to dispatch at run time
+        auto krow = [&](auto i_c, auto ph_c) {
+          constexpr int i = decltype(i_c)::value, PH = decltype(ph_c)::value;
           const int r = b + i;
-          if (i == 4 && !krow_look) break;
+          if (i == 4 && !krow_look) return;
           T v[NV];
-          loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
+          if constexpr (PH >= 0) loadVc<T, NV, PH>(S + r * PITCH, wb, v);
+          else loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
           const bool masked = !jodd && !(r & 1);
           k2row(v, masked, P2 + r * P2W);
           if (REC && masked && i < 4 && rown[i] && j >= 2 * ka && j < 2 * kb) {
@@ -412,6 +441,31 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
             for (int c = 0; c < CPL; ++c)
               if (cvalid[c]) gd[c] = v[2 + 2 * c];
           }
+        };
+        auto krows = [&](auto phb_c) {
+          constexpr int P = decltype(phb_c)::value;
+          auto ph = [](auto ic) { return IC<P < 0 ? -1 : (P + decltype(ic)::value) & (V - 1)>{}; };
+          krow(IC<0>{}, ph(IC<0>{}));
+          krow(IC<1>{}, ph(IC<1>{}));
+          krow(IC<2>{}, ph(IC<2>{}));
+          krow(IC<3>{}, ph(IC<3>{}));
+          krow(IC<4>{}, ph(IC<4>{}));
+        };
+        if (ph_regular) {
+          const int phb = (phj + b * e2m) & (V - 1);
+          if constexpr (V == 2) {
+            if (phb == 0) krows(IC<0>{});
+            else krows(IC<1>{});
+          } else {
+            switch (phb) {
+              case 0: krows(IC<0>{}); break;
+              case 1: krows(IC<1>{}); break;
+              case 2: krows(IC<2>{}); break;
+              default: krows(IC<3>{}); break;
+            }
+          }
+        } else {
+          krows(IC<-1>{});
         }
       } else {
         // decompose, even plane j: K path, coefficients of j and of the odd
@@ -425,51 +479,87 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
         T* orow_e = coef_out + (j * e1 + wr0 + b) * e2 + wc0 + wb + 2;
         T* orow_o = orow_e - plane_sz;
         T A2e[3][NCELL];  // dim-2 interpolants of the even rows b, b+2, b+4
-        // row order b, b+2, b+1, b+4, b+3: odd rows see both even neighbours
-#pragma unroll
-        for (int step = 0; step < 5; ++step) {
-          const int i = step == 0 ? 0 : step == 1 ? 2 : step == 2 ? 1 : step == 3 ? 4 : 3;
+        // row order b, b+2, b+1, b+4, b+3: odd rows see both even neighbours.
+        // One step per row; PH / PHO: the row's phase in plane j / j-1, or -1 to
+        // dispatch at run time.
+        auto step_row = [&](auto step_c, auto ph_c, auto pho_c) {
+          constexpr int step = decltype(step_c)::value;
+          constexpr int i = step == 0 ? 0 : step == 1 ? 2 : step == 2 ? 1 : step == 3 ? 4 : 3;
+          constexpr int PH = decltype(ph_c)::value, PHO = decltype(pho_c)::value;
           const int r = b + i;
           T v[NV];
-          loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
+          if constexpr (PH >= 0) loadVc<T, NV, PH>(S + r * PITCH, wb, v);
+          else loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
           if (i < 4 || krow_look) k2row(v, false, P2 + r * P2W);
-          if (!(i & 1)) {
+          if constexpr (!(i & 1)) {
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
               A2e[i >> 1][2 * c] = v[2 + 2 * c];
               A2e[i >> 1][2 * c + 1] = hl[c] * v[2 + 2 * c] + hr[c] * v[4 + 2 * c];
             }
           }
-          if (i == 4) continue;
-          T A1[NCELL];
+          if constexpr (i != 4) {
+            T A1[NCELL];
 #pragma unroll
-          for (int k = 0; k < NCELL; ++k)
-            A1[k] = (i & 1) ? w1l[i >> 1] * A2e[i >> 1][k] + w1r[i >> 1] * A2e[(i >> 1) + 1][k]
-                            : A2e[i >> 1][k];
-          if (rown[i]) {
-            if (own_e) {
-              T* o = orow_e + int64_t(i) * e2;
+            for (int k = 0; k < NCELL; ++k)
+              A1[k] = (i & 1) ? w1l[i >> 1] * A2e[i >> 1][k] + w1r[i >> 1] * A2e[(i >> 1) + 1][k]
+                              : A2e[i >> 1][k];
+            if (rown[i]) {
+              if (own_e) {
+                T* o = orow_e + int64_t(i) * e2;
 #pragma unroll
-              for (int k = 0; k < NCELL; ++k) {
-                const T cv = v[2 + k] - A1[k];
-                bad = cv * T(0) + bad;
-                if (cvalid[k >> 1]) o[k] = cv;
+                for (int k = 0; k < NCELL; ++k) {
+                  const T cv = v[2 + k] - A1[k];
+                  bad = cv * T(0) + bad;
+                  if (cvalid[k >> 1]) o[k] = cv;
+                }
+              }
+              if (own_o) {
+                T u[NV];
+                if constexpr (PHO >= 0) loadVc<T, NV, PHO>(So + r * PITCH, wb, u);
+                else loadV<T, NV>(So + r * PITCH, rph(phm, r), wb, u);
+                T* o = orow_o + int64_t(i) * e2;
+#pragma unroll
+                for (int k = 0; k < NCELL; ++k) {
+                  const T cv = u[2 + k] - (w0l * A1p[i][k] + w0r * A1[k]);
+                  bad = cv * T(0) + bad;
+                  if (cvalid[k >> 1]) o[k] = cv;
+                }
               }
             }
-            if (own_o) {
-              T u[NV];
-              loadV<T, NV>(So + r * PITCH, rph(phm, r), wb, u);
-              T* o = orow_o + int64_t(i) * e2;
 #pragma unroll
-              for (int k = 0; k < NCELL; ++k) {
-                const T cv = u[2 + k] - (w0l * A1p[i][k] + w0r * A1[k]);
-                bad = cv * T(0) + bad;
-                if (cvalid[k >> 1]) o[k] = cv;
-              }
+            for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[k];
+          }
+        };
+        // 2^k+1 extents: rows and planes advance the phase by one, bands start on
+        // multiples of four rows, so the five rows' phases follow from plane j's
+        auto steps = [&](auto phb_c) {
+          constexpr int P = decltype(phb_c)::value;
+          auto ph = [](auto ic) { return IC<P < 0 ? -1 : (P + decltype(ic)::value) & (V - 1)>{}; };
+          auto pho = [](auto ic) {
+            return IC<P < 0 ? -1 : (P + V - 1 + decltype(ic)::value) & (V - 1)>{};
+          };
+          step_row(IC<0>{}, ph(IC<0>{}), pho(IC<0>{}));
+          step_row(IC<1>{}, ph(IC<2>{}), pho(IC<2>{}));
+          step_row(IC<2>{}, ph(IC<1>{}), pho(IC<1>{}));
+          step_row(IC<3>{}, ph(IC<4>{}), pho(IC<4>{}));
+          step_row(IC<4>{}, ph(IC<3>{}), pho(IC<3>{}));
+        };
+        if (ph_regular) {
+          const int phb = (phj + b * e2m) & (V - 1);
+          if constexpr (V == 2) {
+            if (phb == 0) steps(IC<0>{});
+            else steps(IC<1>{});
+          } else {
+            switch (phb) {
+              case 0: steps(IC<0>{}); break;
+              case 1: steps(IC<1>{}); break;
+              case 2: steps(IC<2>{}); break;
+              default: steps(IC<3>{}); break;
             }
           }
-#pragma unroll
-          for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[k];
+        } else {
+          steps(IC<-1>{});
         }
       }
     }
