@@ -149,6 +149,38 @@ __device__ __forceinline__ void loadVc(const T* row, int base, T (&v)[NV]) {
 template <int N>
 using IC = std::integral_constant<int, N>;
 
+// The lane's NCELL consecutive coefficients into global memory whose first
+// element has phase P (elements mod 16 bytes): the widest aligned vector
+// stores instead of one store per cell.
+template <class T, int NCELL, int P>
+__device__ __forceinline__ void store_cells(T* o, const T (&cv)[NCELL]) {
+  if constexpr (sizeof(T) == 4) {
+    static_assert(NCELL == 4, "fp32 lanes own four cells");
+    if constexpr (P == 0) {
+      *reinterpret_cast<float4*>(o) = make_float4(cv[0], cv[1], cv[2], cv[3]);
+    } else if constexpr (P == 2) {
+      *reinterpret_cast<float2*>(o) = make_float2(cv[0], cv[1]);
+      *reinterpret_cast<float2*>(o + 2) = make_float2(cv[2], cv[3]);
+    } else if constexpr (P == 1) {
+      o[0] = cv[0];
+      *reinterpret_cast<float2*>(o + 1) = make_float2(cv[1], cv[2]);
+      o[3] = cv[3];
+    } else {
+      o[0] = cv[0];
+      *reinterpret_cast<float2*>(o + 1) = make_float2(cv[1], cv[2]);
+      o[3] = cv[3];
+    }
+  } else {
+    static_assert(NCELL == 2, "fp64 lanes own two cells");
+    if constexpr (P == 0) {
+      *reinterpret_cast<double2*>(o) = make_double2(cv[0], cv[1]);
+    } else {
+      o[0] = cv[0];
+      o[1] = cv[1];
+    }
+  }
+}
+
 // the lane's window values: NV = 2*CPL+3 values starting at window column base
 template <class T, int NV>
 __device__ __forceinline__ void loadV(const T* row, int ph, int base, T (&v)[NV]) {
@@ -309,6 +341,12 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   const int e2m = int(e2 & (V - 1));
   // rows and planes advance the phase by one (every 2^k+1 extent with k >= 2)
   const bool ph_regular = e2m == 1 && (plane_sz & (V - 1)) == 1;
+  // vector coefficient stores: whole tile row owned, and coef_out and U on the
+  // same 16-byte phase (both 16-byte aligned), so a cell's global phase is its
+  // window phase; lanes start their cells on a 16-byte window boundary + 2
+  const bool vstore = DEC && tw2 == TW2 &&
+                      ((reinterpret_cast<uintptr_t>(coef_out) & 15) == 0) && (wb % V) == 0 &&
+                      ((map_off & (V - 1)) == 0);
   const int ph00 = int((wr0 * e2 + wc0) & (V - 1));
   // phase (shared-memory position of window column 0) of row r in a plane of phase phj
   auto plane_ph = [&](int64_t jj) { return int((jj * plane_sz + ph00) & (V - 1)); };
@@ -507,11 +545,25 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
             if (rown[i]) {
               if (own_e) {
                 T* o = orow_e + int64_t(i) * e2;
+                T cv[NCELL];
 #pragma unroll
                 for (int k = 0; k < NCELL; ++k) {
-                  const T cv = v[2 + k] - A1[k];
-                  bad = cv * T(0) + bad;
-                  if (cvalid[k >> 1]) o[k] = cv;
+                  cv[k] = v[2 + k] - A1[k];
+                  bad = cv[k] * T(0) + bad;
+                }
+                // the cells' global phase equals the input's: window phase + 2
+                if constexpr (PH >= 0) {
+                  if (vstore) {
+                    store_cells<T, NCELL, (PH + 2) & (V - 1)>(o, cv);
+                  } else {
+#pragma unroll
+                    for (int k = 0; k < NCELL; ++k)
+                      if (cvalid[k >> 1]) o[k] = cv[k];
+                  }
+                } else {
+#pragma unroll
+                  for (int k = 0; k < NCELL; ++k)
+                    if (cvalid[k >> 1]) o[k] = cv[k];
                 }
               }
               if (own_o) {
@@ -519,11 +571,24 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
                 if constexpr (PHO >= 0) loadVc<T, NV, PHO>(So + r * PITCH, wb, u);
                 else loadV<T, NV>(So + r * PITCH, rph(phm, r), wb, u);
                 T* o = orow_o + int64_t(i) * e2;
+                T cv[NCELL];
 #pragma unroll
                 for (int k = 0; k < NCELL; ++k) {
-                  const T cv = u[2 + k] - (w0l * A1p[i][k] + w0r * A1[k]);
-                  bad = cv * T(0) + bad;
-                  if (cvalid[k >> 1]) o[k] = cv;
+                  cv[k] = u[2 + k] - (w0l * A1p[i][k] + w0r * A1[k]);
+                  bad = cv[k] * T(0) + bad;
+                }
+                if constexpr (PHO >= 0) {
+                  if (vstore) {
+                    store_cells<T, NCELL, (PHO + 2) & (V - 1)>(o, cv);
+                  } else {
+#pragma unroll
+                    for (int k = 0; k < NCELL; ++k)
+                      if (cvalid[k >> 1]) o[k] = cv[k];
+                  }
+                } else {
+#pragma unroll
+                  for (int k = 0; k < NCELL; ++k)
+                    if (cvalid[k >> 1]) o[k] = cv[k];
                 }
               }
             }
