@@ -299,17 +299,20 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
     rc[i] = uint32_t(uint64_t(gr * e2 + wc0 - map_off));
     if (r < RWn && gr >= 0 && gr < e1) rvalid |= 1u << i;
   }
+  const uint32_t raw_s = ptx::smem_addr(raw) + uint32_t(warp * PITCH * sizeof(T));
+  const uint32_t bar_s = ptx::smem_addr(bar);
   auto issue = [&](int64_t jj) {
     const int sl = int(jj - j0) % NS;
     if (tid == 0) ptx::mbar_arrive_expect_tx(&bar[sl], tx_bytes);
     if (ptx::elect_one()) {
-      T* dst = raw + sl * SLOT + warp * PITCH;
+      const uint32_t dst = raw_s + uint32_t(sl * SLOT * sizeof(T));
+      const uint32_t bs = bar_s + uint32_t(sl * sizeof(uint64_t));
       const uint32_t pb = uint32_t(uint64_t(jj * plane_sz));
 #pragma unroll
       for (int i = 0; i < RPW; ++i)
         if (rvalid & (1u << i))
-          ptx::tma_load_1d(dst + i * NW * PITCH, &map, int((pb + rc[i]) & ~uint32_t(V - 1)),
-                           &bar[sl]);
+          ptx::tma_load_1d_s(dst + uint32_t(i * NW * PITCH * sizeof(T)), &map,
+                             int((pb + rc[i]) & ~uint32_t(V - 1)), bs);
     }
   };
 

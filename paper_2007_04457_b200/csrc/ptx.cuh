@@ -105,6 +105,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* map, int x, u
       : "memory");
 }
 
+// tma_load_1d with the shared-memory destination and barrier given as 32-bit
+// shared-window addresses (callers hoist the conversions out of issue loops)
+__device__ __forceinline__ void tma_load_1d_s(uint32_t dst, const void* map, int x, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2}], [%3];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(bar)
+      : "memory");
+}
+
 // 16-byte async copy global -> shared (LDGSTS), L2 only; src_bytes < 16 zero-fills the rest.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
