@@ -16,6 +16,7 @@
 // safe (every cell is read before it is written, by the CTA that owns it).
 // The last fine row and column of the level are the faces of k_interp_face.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 
 #include "kernels.cuh"
@@ -63,6 +64,9 @@ struct ICfg {
   static_assert(total * MINB <= 227 * 1024, "shared memory budget");
 };
 
+template <int N>
+using IC = std::integral_constant<int, N>;
+
 template <class T>
 struct Vec2i;
 template <>
@@ -99,6 +103,34 @@ __device__ __forceinline__ void ldn(const T* row, int pos, T (&v)[N]) {
   } else {
 #pragma unroll
     for (int k = 0; k < N; ++k) v[k] = row[pos + k];
+  }
+}
+
+// ldn with the phase of pos known at compile time (pos - PH is 16-byte aligned)
+template <class T, int N, int PH>
+__device__ __forceinline__ void ldnc(const T* row, int pos, T (&v)[N]) {
+  const T* p = row + (pos - PH);
+  if constexpr (N == 4 && sizeof(T) == 4) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    if constexpr (PH == 0) {
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+      const float4 y = *reinterpret_cast<const float4*>(p + 4);
+      const float w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = w[PH + k];
+    }
+  } else if constexpr (N == 2 && sizeof(T) == 8) {
+    if constexpr (PH == 0) {
+      const double2 x = *reinterpret_cast<const double2*>(p);
+      v[0] = x.x;
+      v[1] = x.y;
+    } else {
+      v[0] = p[1];
+      v[1] = p[2];
+    }
+  } else {
+    ldn<T, N>(row, pos, v);
   }
 }
 
@@ -165,15 +197,18 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
   const uint32_t tx_f = uint32_t(frows) * C::BOX * uint32_t(sizeof(T));
   const int crows = tw1 + 1;
   const uint32_t tx_c = uint32_t(crows) * C::CBOX * uint32_t(sizeof(T)) * (HASZ ? 2u : 1u);
+  const uint32_t ring_s = ptx::smem_addr(ring), cbuf_s = ptx::smem_addr(cbuf);
+  const uint32_t barf_s = ptx::smem_addr(barf), barc_s = ptx::smem_addr(barc);
   auto issue_f = [&](int64_t j) {  // fine plane j into slot (j - jlo) % NS
     const int sl = int(j - jlo) % NS;
     if (tid == 0) ptx::mbar_arrive_expect_tx(&barf[sl], tx_f);
     if (ptx::elect_one()) {
-      T* dst = ring + sl * SLOT;
+      const uint32_t dst = ring_s + uint32_t(sl * SLOT * sizeof(T));
+      const uint32_t bs = barf_s + uint32_t(sl * sizeof(uint64_t));
       const int64_t base = (j * e1 + 2 * q1a) * e2 + 2 * q2a - coef_off;
       for (int r = warp; r < frows; r += NW) {
         const int64_t f = base + int64_t(r) * e2;
-        ptx::tma_load_1d(dst + r * PITCH, &mcoef, int(f & ~int64_t(V - 1)), &barf[sl]);
+        ptx::tma_load_1d_s(dst + uint32_t(r * PITCH * sizeof(T)), &mcoef, int(f & ~int64_t(V - 1)), bs);
       }
     }
   };
@@ -181,13 +216,14 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     const int bsl = int(m & 1);
     if (tid == 0) ptx::mbar_arrive_expect_tx(&barc[bsl], tx_c);
     if (ptx::elect_one()) {
-      T* dst = cbuf + bsl * 2 * CSLOT;
+      const uint32_t dst = cbuf_s + uint32_t(bsl * 2 * CSLOT * sizeof(T));
+      const uint32_t bs = barc_s + uint32_t(bsl * sizeof(uint64_t));
       const int64_t base = (m * c1 + q1a) * c2 + q2a - c_off;
       for (int r = warp; r < crows; r += NW) {
         const int64_t f = base + int64_t(r) * c2;
         const int x = int(f & ~int64_t(V - 1));
-        ptx::tma_load_1d(dst + r * CPITCH, &mC, x, &barc[bsl]);
-        if (HASZ) ptx::tma_load_1d(dst + CSLOT + r * CPITCH, &mZ, x, &barc[bsl]);
+        ptx::tma_load_1d_s(dst + uint32_t(r * CPITCH * sizeof(T)), &mC, x, bs);
+        if (HASZ) ptx::tma_load_1d_s(dst + uint32_t((CSLOT + r * CPITCH) * sizeof(T)), &mZ, x, bs);
       }
     }
   };
@@ -209,6 +245,13 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
   if (ka + 1 <= kb) issue_c(ka + 1);
 
   const int e2m = int(e2 & (V - 1)), c2m = int(c2 & (V - 1));
+  // 2^k+1 extents: consecutive fine rows advance the phase by one (fp64 only:
+  // the fp32 march is at its bandwidth bound and measured no gain)
+  const bool ph_regular = sizeof(T) == 8 && e2m == 1;
+  // vector output stores: whole tile row owned, output and coefficient map base
+  // on the same 16-byte phase (cell phases then follow fpos)
+  const bool vstore = tw2 == TW2 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                      (coef_off & (V - 1)) == 0 && (2 * t0) % V == 0;
   const int fph0 = int((2 * q1a * e2 + 2 * q2a) & (V - 1));
   const int cph0 = int((q1a * c2 + q2a) & (V - 1));
   auto fpos = [&](int64_t j, int r) {
@@ -232,24 +275,57 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     if (WITH) ptx::mbar_wait(&barf[p % NS], uint32_t((p / NS) & 1));
     if (!has_band) return;
     T* o = obase + j * plane_f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    // one row; PH: the phase of the row's cells (compile time), or -1
+    auto row = [&](auto i_c, auto ph_c) {
+      constexpr int i = decltype(i_c)::value, PH = decltype(ph_c)::value;
       T v[NCELL];
 #pragma unroll
       for (int k = 0; k < NCELL; ++k) v[k] = odd ? w0l * A1p[i][k] + w0r * A1[i][k] : A1[i][k];
       if (WITH) {
         T cf[NCELL];
-        ldn<T, NCELL>(S + (b + i) * PITCH, fpos(j, b + i), cf);
+        if constexpr (PH >= 0) ldnc<T, NCELL, PH>(S + (b + i) * PITCH, fpos(j, b + i), cf);
+        else ldn<T, NCELL>(S + (b + i) * PITCH, fpos(j, b + i), cf);
 #pragma unroll
         for (int k = 0; k < NCELL; ++k)
           // the coarse nodes (even plane, even row, even column) keep the interpolant
           if (odd || (i & 1) || (k & 1)) v[k] += cf[k];
       }
       if (rown[i]) {
+        // the output has the coefficients' layout: same phase when both are aligned
+        if constexpr (PH >= 0) {
+          if (vstore) {
+            store_cells<T, NCELL, PH>(o + int64_t(i) * e2, v);
+            return;
+          }
+        }
 #pragma unroll
         for (int k = 0; k < NCELL; ++k)
           if (cvalid[k >> 1]) o[int64_t(i) * e2 + k] = v[k];
       }
+    };
+    auto rows4 = [&](auto phb_c) {
+      constexpr int P = decltype(phb_c)::value;
+      auto ph = [](auto ic) { return IC<P < 0 ? -1 : (P + decltype(ic)::value) & (V - 1)>{}; };
+      row(IC<0>{}, ph(IC<0>{}));
+      row(IC<1>{}, ph(IC<1>{}));
+      row(IC<2>{}, ph(IC<2>{}));
+      row(IC<3>{}, ph(IC<3>{}));
+    };
+    if (ph_regular) {
+      const int phb = fpos(j, b) & (V - 1);
+      if constexpr (V == 2) {
+        if (phb == 0) rows4(IC<0>{});
+        else rows4(IC<1>{});
+      } else {
+        switch (phb) {
+          case 0: rows4(IC<0>{}); break;
+          case 1: rows4(IC<1>{}); break;
+          case 2: rows4(IC<2>{}); break;
+          default: rows4(IC<3>{}); break;
+        }
+      }
+    } else {
+      rows4(IC<-1>{});
     }
   };
 

@@ -149,38 +149,6 @@ __device__ __forceinline__ void loadVc(const T* row, int base, T (&v)[NV]) {
 template <int N>
 using IC = std::integral_constant<int, N>;
 
-// The lane's NCELL consecutive coefficients into global memory whose first
-// element has phase P (elements mod 16 bytes): the widest aligned vector
-// stores instead of one store per cell.
-template <class T, int NCELL, int P>
-__device__ __forceinline__ void store_cells(T* o, const T (&cv)[NCELL]) {
-  if constexpr (sizeof(T) == 4) {
-    static_assert(NCELL == 4, "fp32 lanes own four cells");
-    if constexpr (P == 0) {
-      *reinterpret_cast<float4*>(o) = make_float4(cv[0], cv[1], cv[2], cv[3]);
-    } else if constexpr (P == 2) {
-      *reinterpret_cast<float2*>(o) = make_float2(cv[0], cv[1]);
-      *reinterpret_cast<float2*>(o + 2) = make_float2(cv[2], cv[3]);
-    } else if constexpr (P == 1) {
-      o[0] = cv[0];
-      *reinterpret_cast<float2*>(o + 1) = make_float2(cv[1], cv[2]);
-      o[3] = cv[3];
-    } else {
-      o[0] = cv[0];
-      *reinterpret_cast<float2*>(o + 1) = make_float2(cv[1], cv[2]);
-      o[3] = cv[3];
-    }
-  } else {
-    static_assert(NCELL == 2, "fp64 lanes own two cells");
-    if constexpr (P == 0) {
-      *reinterpret_cast<double2*>(o) = make_double2(cv[0], cv[1]);
-    } else {
-      o[0] = cv[0];
-      o[1] = cv[1];
-    }
-  }
-}
-
 // the lane's window values: NV = 2*CPL+3 values starting at window column base
 template <class T, int NV>
 __device__ __forceinline__ void loadV(const T* row, int ph, int base, T (&v)[NV]) {
