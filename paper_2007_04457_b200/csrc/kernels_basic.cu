@@ -198,37 +198,45 @@ __global__ void __launch_bounds__(128) k_thomas(T* z, int64_t n0, int64_t n1, in
 
 // ---- gathers / scatters ------------------------------------------------------
 
-// Row-wise gathers / scatters: a warp per row of the compact array (one index
-// division per row, consecutive lanes on consecutive elements).
+// Row-wise gathers / scatters: a warp per segment of up to kRowSeg elements of a
+// row of the compact array (one index division per segment, consecutive lanes
+// on consecutive elements; long rows -- 1D grids -- spread over many warps).
+constexpr int64_t kRowSeg = 1024;
+
 template <class T>
 __global__ void __launch_bounds__(256) k_gather(const T* __restrict__ src, int64_t s1, int64_t s2,
                                                 int64_t stride, T* __restrict__ dst, int64_t d0,
                                                 int64_t d1, int64_t d2) {
-  const int64_t rows = d0 * d1;
+  const int64_t nseg = (d2 + kRowSeg - 1) / kRowSeg, items = d0 * d1 * nseg;
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  for (int64_t row = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); row < rows;
-       row += int64_t(gridDim.x) * wpb) {
+  for (int64_t it = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); it < items;
+       it += int64_t(gridDim.x) * wpb) {
+    const int64_t row = it / nseg, seg = it - row * nseg;
     const int64_t q0 = row / d1, q1 = row - q0 * d1;
     const T* sr = src + ((q0 * stride) * s1 + q1 * stride) * s2;
     T* dr = dst + row * d2;
-    for (int64_t q2 = lane; q2 < d2; q2 += 32) dr[q2] = sr[q2 * stride];
+    const int64_t hi = (seg + 1) * kRowSeg < d2 ? (seg + 1) * kRowSeg : d2;
+    for (int64_t q2 = seg * kRowSeg + lane; q2 < hi; q2 += 32) dr[q2] = sr[q2 * stride];
   }
 }
 
 template <class T>
 __global__ void __launch_bounds__(256) k_scatter_even(const T* __restrict__ src, T* __restrict__ dst,
                                                       LevelArgs<T> a) {
-  const int64_t c1 = a.c[1], c2 = a.c[2], rows = a.c[0] * c1;
+  const int64_t c1 = a.c[1], c2 = a.c[2];
+  const int64_t nseg = (c2 + kRowSeg - 1) / kRowSeg, items = a.c[0] * c1 * nseg;
   const int64_t e1 = a.e[1], e2 = a.e[2];
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
-  for (int64_t row = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); row < rows;
-       row += int64_t(gridDim.x) * wpb) {
+  for (int64_t it = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); it < items;
+       it += int64_t(gridDim.x) * wpb) {
+    const int64_t row = it / nseg, seg = it - row * nseg;
     const int64_t q0 = row / c1, q1 = row - q0 * c1;
     const T* sr = src + row * c2;
     T* dr = dst + ((2 * q0) * e1 + 2 * q1) * e2;
-    for (int64_t q2 = lane; q2 < c2; q2 += 32) dr[2 * q2] = sr[q2];
+    const int64_t hi = (seg + 1) * kRowSeg < c2 ? (seg + 1) * kRowSeg : c2;
+    for (int64_t q2 = seg * kRowSeg + lane; q2 < hi; q2 += 32) dr[2 * q2] = sr[q2];
   }
 }
 
@@ -363,12 +371,13 @@ template <class T>
 void launch_gather(const T* src, const int64_t se[3], int64_t stride, T* dst,
                    const int64_t de[3], cudaStream_t s) {
   // a warp per destination row
-  LAUNCH(k_gather<T>, de[0] * de[1] * 32, 256, s, src, se[1], se[2], stride, dst, de[0],
-         de[1], de[2]);
+  const int64_t items = de[0] * de[1] * ((de[2] + kRowSeg - 1) / kRowSeg);  // a warp each
+  LAUNCH(k_gather<T>, items * 32, 256, s, src, se[1], se[2], stride, dst, de[0], de[1], de[2]);
 }
 template <class T>
 void launch_scatter_even(const T* src, T* dst, const LevelArgs<T>& a, cudaStream_t s) {
-  LAUNCH(k_scatter_even<T>, a.c[0] * a.c[1] * 32, 256, s, src, dst, a);  // a warp per row
+  const int64_t items = a.c[0] * a.c[1] * ((a.c[2] + kRowSeg - 1) / kRowSeg);  // a warp each
+  LAUNCH(k_scatter_even<T>, items * 32, 256, s, src, dst, a);
 }
 template <class T>
 void launch_coefficients(const T* fine, T* coeffs, const LevelArgs<T>& a, cudaStream_t s) {

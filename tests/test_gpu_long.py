@@ -78,3 +78,30 @@ def test_long_lines_vs_reference(cuda, shape, dt, nonuniform):
     plan.recompose_into(ref_p, y, m)
     err_m = float(np.abs(y.cpu().numpy().astype(np.float64) - want).max()) / scale
     assert err_m <= tol, f"recompose(upto {m}) vs {O.kind}: {err_m:.3e}"
+
+
+@pytest.mark.parametrize("shape,dt,limit_ms", [(((1 << 24) + 1,), "f64", 25.0),
+                                                ((4097, 4097), "f32", 15.0),
+                                                ((129, 129, 4097), "f32", 25.0)],
+                         ids=["line_2^24+1_f64", "4097^2_f32", "129x129x4097_f32"])
+def test_long_shapes_time_bound(cuda, shape, dt, limit_ms):
+    """Guard against a serial fallback on long lines (a warp or a thread per
+    line of millions of nodes): loose bounds, ~10x above the measured times."""
+    import torch
+    import paper_2007_04457_b200 as hgr
+    g = hgr.GridHierarchy.uniform(list(shape))
+    plan = hgr.Plan(g, dt)
+    x = hgr.synthetic_field(list(shape), dt, seed=5, device=cuda)
+    p, y = torch.empty_like(x), torch.empty_like(x)
+    for _ in range(2):
+        plan.decompose_into(x, p)
+        plan.recompose_into(p, y, g.levels())
+    torch.cuda.synchronize(cuda)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    plan.decompose_into(x, p)
+    plan.recompose_into(p, y, g.levels())
+    ev1.record()
+    torch.cuda.synchronize(cuda)
+    ms = ev0.elapsed_time(ev1)
+    assert ms < limit_ms, f"round trip {ms:.2f} ms"
