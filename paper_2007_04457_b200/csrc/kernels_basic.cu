@@ -5,6 +5,8 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#include "launch.cuh"
+#include "ptx.cuh"
 #include "plan.hpp"
 
 namespace hgrb {
@@ -207,6 +209,8 @@ template <class T>
 __global__ void __launch_bounds__(256) k_gather(const T* __restrict__ src, int64_t s1, int64_t s2,
                                                 int64_t stride, T* __restrict__ dst, int64_t d0,
                                                 int64_t d1, int64_t d2) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int64_t nseg = (d2 + kRowSeg - 1) / kRowSeg, items = d0 * d1 * nseg;
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
@@ -224,6 +228,8 @@ __global__ void __launch_bounds__(256) k_gather(const T* __restrict__ src, int64
 template <class T>
 __global__ void __launch_bounds__(256) k_scatter_even(const T* __restrict__ src, T* __restrict__ dst,
                                                       LevelArgs<T> a) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int64_t c1 = a.c[1], c2 = a.c[2];
   const int64_t nseg = (c2 + kRowSeg - 1) / kRowSeg, items = a.c[0] * c1 * nseg;
   const int64_t e1 = a.e[1], e2 = a.e[2];
@@ -372,12 +378,15 @@ void launch_gather(const T* src, const int64_t se[3], int64_t stride, T* dst,
                    const int64_t de[3], cudaStream_t s) {
   // a warp per destination row
   const int64_t items = de[0] * de[1] * ((de[2] + kRowSeg - 1) / kRowSeg);  // a warp each
-  LAUNCH(k_gather<T>, items * 32, 256, s, src, se[1], se[2], stride, dst, de[0], de[1], de[2]);
+  launch_pdl(k_gather<T>, dim3(grid_for(items * 32, 256)), dim3(256), 0, s, 8 * de[0] * de[1] * de[2],
+             src, se[1], se[2], stride,
+             dst, de[0], de[1], de[2]);
 }
 template <class T>
 void launch_scatter_even(const T* src, T* dst, const LevelArgs<T>& a, cudaStream_t s) {
   const int64_t items = a.c[0] * a.c[1] * ((a.c[2] + kRowSeg - 1) / kRowSeg);  // a warp each
-  LAUNCH(k_scatter_even<T>, items * 32, 256, s, src, dst, a);
+  launch_pdl(k_scatter_even<T>, dim3(grid_for(items * 32, 256)), dim3(256), 0, s,
+             a.e[0] * a.e[1] * a.e[2], src, dst, a);
 }
 template <class T>
 void launch_coefficients(const T* fine, T* coeffs, const LevelArgs<T>& a, cudaStream_t s) {

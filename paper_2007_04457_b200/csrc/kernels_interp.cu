@@ -23,6 +23,7 @@
 #include "kernels_fused.cuh"
 #include "plan.hpp"
 #include "ptx.cuh"
+#include "launch.cuh"
 #include "tma.hpp"
 
 namespace hgrb {
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
                    T* __restrict__ out, LevelArgs<T> a, int S0, int nt1, int nt2, int nseg,
                    int seg_base) {
   using C = ICfg<T>;
+  ptx::pdl_trigger();
   constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NW = C::NW;
   constexpr int TW1 = C::TW1, TW2 = C::TW2, WG = C::WG, NB = C::NB;
   constexpr int CPITCH = C::CPITCH, CSLOT = C::CSLOT, CPL = C::CPL, NCELL = C::NCELL;
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  ptx::pdl_wait();  // C, Z and the coefficients come from earlier launches
   if (WITH)
     for (int64_t j = jlo; j <= jhi && j < jlo + NS; ++j) issue_f(j);
   issue_c(ka);
@@ -388,6 +391,8 @@ template <class T>
 __global__ void __launch_bounds__(256)
     k_interp_face(const T* coef, T* out, const T* __restrict__ C, const T* __restrict__ Z,
                   LevelArgs<T> a, bool with) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int e1 = int(a.e[1]), e2 = int(a.e[2]);
   const int c1 = int(a.c[1]), c2 = int(a.c[2]);
   const int j = blockIdx.x, face = blockIdx.y;
@@ -465,7 +470,7 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
     mcoef = mC;
     if (WITH) make_tma_1d(&mcoef, coef + coef_off, uint64_t(Nf - coef_off), int(sizeof(T)), Cf::BOX);
     const int64_t blocks = tiles * (sb - sa);
-    kern<<<unsigned(blocks), Cf::NT, Cf::total, s>>>(mcoef, mC, mZ, coef_off, c_off, out, a, S0,
+    launch_pdl(kern, dim3(unsigned(blocks)), dim3(Cf::NT), Cf::total, s, Nf, mcoef, mC, mZ, coef_off, c_off, out, a, S0,
                                                      nt1, nt2, nseg, sa);
     HGR_CUDA_CHECK(cudaGetLastError());
     sa = sb;
@@ -486,8 +491,7 @@ bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const Leve
   else if (with) run_interp<T, true, false>(coef, out, C, Z, a, s, s0);
   else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s, s0);
   else run_interp<T, false, false>(coef, out, C, Z, a, s, s0);
-  k_interp_face<T><<<dim3(unsigned(a.e[0]), 2, unsigned((std::max(a.e[1], a.e[2]) + 255) / 256)),
-                     256, 0, s>>>(coef, out, C, Z, a, with);
+  launch_pdl(k_interp_face<T>, dim3(unsigned(a.e[0]), 2, unsigned((std::max(a.e[1], a.e[2]) + 255) / 256)), dim3(256), 0, s, a.e[0] * a.e[1] * a.e[2], coef, out, C, Z, a, with);
   HGR_CUDA_CHECK(cudaGetLastError());
   return true;
 }

@@ -47,6 +47,7 @@
 #include "kernels_fused.cuh"
 #include "plan.hpp"
 #include "ptx.cuh"
+#include "launch.cuh"
 #include "tma.hpp"
 
 namespace hgrb {
@@ -172,6 +173,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
                   int nt2, int nseg, int seg_base, int* flag) {
   using C = LCfg<T>;
   using T2 = typename Vec2<T>::type;
+  ptx::pdl_trigger();
   constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NT = C::NT;
   constexpr int TW1 = C::TW1, TW2 = C::TW2, P2W = C::P2W, NW = C::NW, NB = C::NB, WG = C::WG;
   constexpr int CPL = C::CPL, NCELL = C::NCELL, NV = C::NV, CQ = C::CQ;
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   }
   __syncthreads();
   const int nplanes = int(jend - j0 + 1);
+  ptx::pdl_wait();  // U is the previous launches' output
   for (int p = 0; p < nplanes && p < NS; ++p) issue(j0 + p);
 
   const int e2m = int(e2 & (V - 1));
@@ -636,6 +639,8 @@ __global__ void __launch_bounds__(256)
     k_level_face(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ zload,
                  T* __restrict__ gather, LevelArgs<T> a, int* flag) {
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_f[];
   T* Rs = reinterpret_cast<T*>(smem_f);  // [5][e] partial sums
   const int e0 = int(a.e[0]), e1 = int(a.e[1]), e2 = int(a.e[2]);
@@ -783,9 +788,8 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
     CUtensorMap map;
     make_tma_1d(&map, U + map_off, uint64_t(N - map_off), int(sizeof(T)), C::BOX);
     const int64_t blocks = tiles * (sb - sa);
-    kern<<<unsigned(blocks), C::NT, C::total, s>>>(map, map_off, coef, z, gather, a, S0, nt1, nt2,
-                                                   nseg, sa, flag);
-    HGR_CUDA_CHECK(cudaGetLastError());
+    launch_pdl(kern, dim3(unsigned(blocks)), dim3(C::NT), C::total, s, N, map, map_off, coef, z,
+               gather, a, S0, nt1, nt2, nseg, sa, flag);
     sa = sb;
   }
   const int64_t fseg =
@@ -795,8 +799,8 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
                    unsigned(fseg));
   const size_t fsmem = size_t(5) * size_t(2 * kFaceSeg + 3) * sizeof(T);
   set_level_face_smem<T, MODE>(fsmem);
-  k_level_face<T, MODE><<<fgrid, 256, fsmem, s>>>(U, coef, z, gather, a, flag);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(k_level_face<T, MODE>, fgrid, dim3(256), fsmem, s, a.e[0] * a.e[1] * a.e[2], U, coef,
+             z, gather, a, flag);
 }
 
 }  // namespace

@@ -13,6 +13,8 @@
 // on k_thomas_long (kernels_thomas.cu).
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
+#include "launch.cuh"
+#include "ptx.cuh"
 #include "plan.hpp"
 
 namespace hgrb {
@@ -32,6 +34,8 @@ __global__ void __launch_bounds__(256)
                  T* __restrict__ gather, const T* __restrict__ taps, const T* __restrict__ wl,
                  const T* __restrict__ wr, int64_t n, int64_t nc, int* flag) {
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   bool bad = false;
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nc;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -70,6 +74,8 @@ template <class T, bool WITH, bool HASZ>
 __global__ void __launch_bounds__(256)
     k_line_interp(const T* coef, T* out, const T* __restrict__ C, const T* __restrict__ Z,
                   const T* __restrict__ wl, const T* __restrict__ wr, int64_t nc) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nc;
        q += int64_t(gridDim.x) * blockDim.x) {
     const T c0 = HASZ ? C[q] - Z[q] : C[q];
@@ -89,18 +95,18 @@ template <class T, int MODE>
 void run_line(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int* flag,
               cudaStream_t s) {
   const int64_t nc = a.c[2];
-  k_line_level<T, MODE><<<grid_for(nc, 256), 256, 0, s>>>(U, coef, z, gather, a.taps[2], a.wl[2],
-                                                          a.wr[2], a.e[2], nc, flag);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(k_line_level<T, MODE>, dim3(grid_for(nc, 256)), dim3(256), 0, s, a.e[2], U, coef, z,
+             gather,
+             a.taps[2], a.wl[2], a.wr[2], a.e[2], nc, flag);
 }
 
 template <class T, bool WITH, bool HASZ>
 void run_line_interp(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
                      cudaStream_t s) {
   const int64_t nc = a.c[2];
-  k_line_interp<T, WITH, HASZ><<<grid_for(nc, 256), 256, 0, s>>>(coef, out, C, Z, a.wl[2],
-                                                                 a.wr[2], nc);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(k_line_interp<T, WITH, HASZ>, dim3(grid_for(nc, 256)), dim3(256), 0, s, a.e[2], coef,
+             out, C, Z,
+             a.wl[2], a.wr[2], nc);
 }
 
 }  // namespace

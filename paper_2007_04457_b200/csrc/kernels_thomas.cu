@@ -25,6 +25,7 @@
 #include <type_traits>
 
 #include "kernels_fused.cuh"
+#include "launch.cuh"
 #include "plan.hpp"
 #include "ptx.cuh"
 
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     k_thomas_lines(const T* in, T* out, int n, int sd, int so, int na, int c2, int nfull,
                    int ntail, int nlg, int S, int J, const T* __restrict__ mult,
                    const T* __restrict__ rpiv, const T* __restrict__ upper) {
+  ptx::pdl_trigger();
   constexpr int NT = 32 * kLW, NC = kLW, GW = 32 * LPT;
   constexpr int CHP = chunk_pitch<T, CH>(), NTB = NC * CHP;
   constexpr int H = window_halo<T>();
@@ -388,6 +390,7 @@ __global__ void __launch_bounds__(32 * kLW, 1)
     }
   };
   int g = blockIdx.x;
+  ptx::pdl_wait();  // the lines are the previous launches' output
   if (g < ngroups) {
     if constexpr (RP) prefetch_regs(g);
     else prefetch(g);
@@ -526,6 +529,7 @@ __global__ void __launch_bounds__(512, 1)
     k_thomas_rows(const T* in, T* out, int64_t rows, int n, const T* __restrict__ mult,
                   const T* __restrict__ rpiv, const T* __restrict__ upper) {
   using C = RowsCfg<T, CH, R, STAGE>;
+  ptx::pdl_trigger();
   constexpr int NC = C::NC, CPW = C::CPW, CHP = C::CHP, NTB = C::NTB;
   extern __shared__ __align__(16) unsigned char smem_t[];
   T* tm = reinterpret_cast<T*>(smem_t);
@@ -565,6 +569,7 @@ __global__ void __launch_bounds__(512, 1)
   };
   int64_t g = blockIdx.x;
   const int64_t G = gridDim.x;
+  ptx::pdl_wait();
   if (tid == 0) {
     if (g < ngroups) load(g, 0);
     if (g + G < ngroups) load(g + G, 1);
@@ -633,6 +638,7 @@ __global__ void __launch_bounds__(512, 1)
                   const T* __restrict__ mult, const T* __restrict__ rpiv,
                   const T* __restrict__ upper) {
   using C = LongCfg<T, CH>;
+  ptx::pdl_trigger();
   constexpr int NT = C::NT, NC = C::NC, TILE = C::TILE;
   constexpr int H = window_halo<T>();
   extern __shared__ __align__(16) unsigned char smem_t[];
@@ -662,6 +668,7 @@ __global__ void __launch_bounds__(512, 1)
   T tm[CH], tp[CH], tu[CH];
   int64_t cur_j = -1;
   int64_t g = blockIdx.x;
+  ptx::pdl_wait();
   if (g < ngroups) prefetch(g, 0);
   for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
     const int b = it & 1;
@@ -763,8 +770,8 @@ void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int64_t groups = (rows + R - 1) / R;
   const int grid = int(groups < sm_count() ? groups : sm_count());
-  kern<<<grid, C::NT, smem, s>>>(in, out, rows, int(n), mult, rpiv, upper);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(kern, dim3(grid), dim3(C::NT), smem, s, 8 * rows * n, in, out, rows, int(n), mult, rpiv,
+             upper);
 }
 
 template <class T, int CH, bool WIN>
@@ -791,9 +798,9 @@ void run_lines(const T* in, T* out, const int64_t e[3], int dim, const T* mult, 
   const int J = (n + S - 1) / S;
   const int64_t groups = int64_t(nlg) * J;
   const int grid = int(groups < sm_count() ? groups : sm_count());
-  kern<<<grid, NT, smem, s>>>(in, out, n, sd, so, na, c2, nfull, ntail, nlg, S, J, mult, rpiv,
-                              upper);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(kern, dim3(grid), dim3(NT), smem, s, 8 * e[0] * e[1] * e[2], in, out, n, sd, so, na, c2,
+             nfull, ntail, nlg, S,
+             J, mult, rpiv, upper);
 }
 
 template <class T, int CH>
@@ -806,8 +813,9 @@ void run_long(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const
   set_smem_attr(reinterpret_cast<const void*>(kern), C::smem());
   const int64_t groups = rows * J;
   const int grid = int(groups < sm_count() ? groups : sm_count());
-  kern<<<grid, C::NT, C::smem(), s>>>(in, out, rows, n, S, J, mult, rpiv, upper);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  launch_pdl(kern, dim3(grid), dim3(C::NT), C::smem(), s, 8 * rows * n, in, out, rows, n, S, J, mult,
+             rpiv,
+             upper);
 }
 
 // longest rows of the register-tiled row kernels; longer rows take k_thomas_long

@@ -115,6 +115,16 @@ __device__ __forceinline__ void tma_load_1d_s(uint32_t dst, const void* map, int
       : "memory");
 }
 
+// Programmatic dependent launch (kernels launched with the programmatic
+// stream-serialization attribute, launch.cuh): the next kernel in the stream
+// may be scheduled once every CTA of this one has called pdl_trigger; its CTAs
+// run their prologue and block in pdl_wait until this grid has completed and
+// its memory is visible. Both are no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 16-byte async copy global -> shared (LDGSTS), L2 only; src_bytes < 16 zero-fills the rest.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
