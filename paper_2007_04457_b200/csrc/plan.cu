@@ -346,6 +346,9 @@ class PlanT final : public Plan {
 template <class T>
 PlanT<T>::PlanT(const Hierarchy& hier) {
   h = hier;
+  // 1D/2D levels are a few rows of fused tiles: the fused path wins from 4096
+  // nodes (with programmatic launches), 3D levels from 2^15 (measured)
+  big_nodes_ = h.rank == 3 ? std::size_t(1) << 15 : std::size_t(4096);
   if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   s0_dec_.assign(std::size_t(h.L) + 1, 0);
