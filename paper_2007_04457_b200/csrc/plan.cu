@@ -333,6 +333,7 @@ class PlanT final : public Plan {
   // coarse tail: levels 1..tail_lt_ (all below the fused threshold, under the
   // top) run as one single-CTA launch per direction (kernels_tail.cu)
   int tail_lt_ = 0;
+  bool auto_tune_pending_ = false;  // HGR_AUTOTUNE=1
   TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
   std::vector<int> s0_dec_, s0_rec_, s0_int_;
@@ -350,6 +351,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   // nodes (with programmatic launches), 3D levels from 2^15 (measured)
   big_nodes_ = h.rank == 3 ? std::size_t(1) << 15 : std::size_t(4096);
   if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
+  if (const char* v = std::getenv("HGR_AUTOTUNE")) auto_tune_pending_ = v[0] == '1';
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   s0_dec_.assign(std::size_t(h.L) + 1, 0);
   s0_rec_.assign(std::size_t(h.L) + 1, 0);
@@ -693,6 +695,12 @@ void PlanT<T>::assemble(T* out, cudaStream_t s) {
 template <class T>
 void PlanT<T>::decompose_to(const void* d_in, void* d_out, cudaStream_t s) {
   if (d_in == d_out) return decompose(d_out, s);
+  // HGR_AUTOTUNE=1: tune on the first out-of-place decompose (its output is
+  // about to be overwritten anyway), for callers that never call autotune()
+  if (auto_tune_pending_) {
+    auto_tune_pending_ = false;
+    if (!profiling_) autotune(d_in, d_out, s);
+  }
   run_graphed(0, d_in, d_out, 0, s, [&](cudaStream_t st) { decompose_to_direct(d_in, d_out, st); });
 }
 

@@ -64,3 +64,29 @@ def test_autotune_report_and_bitwise_results(cuda, shape, dt):
     p2 = torch.empty_like(x)
     plan.decompose_into(x, p2)
     assert torch.equal(p0, p2)
+
+
+def test_env_autotune_first_decompose(cuda):
+    """HGR_AUTOTUNE=1: the first out-of-place decompose tunes the plan first and
+    still returns the right pyramid (bit-identical to an untuned plan)."""
+    import os
+    import torch
+    import paper_2007_04457_b200 as hgr
+    shape = [129, 129, 257]
+    g = hgr.GridHierarchy.uniform(shape)
+    x = hgr.synthetic_field(shape, "f32", seed=11, device=cuda)
+    ref = torch.empty_like(x)
+    hgr.Plan(g, "f32").decompose_into(x, ref)
+    old = os.environ.get("HGR_AUTOTUNE")
+    os.environ["HGR_AUTOTUNE"] = "1"
+    try:
+        plan = hgr.Plan(g, "f32")
+    finally:
+        if old is None:
+            del os.environ["HGR_AUTOTUNE"]
+        else:
+            os.environ["HGR_AUTOTUNE"] = old
+    out = torch.empty_like(x)
+    plan.decompose_into(x, out)
+    plan.sync_status()
+    assert torch.equal(out, ref)
