@@ -60,9 +60,12 @@ int hgr_cuda_abi_version(void);
 /* ---- plans: GridHierarchy + device tables + workspace ---------------------
  * Replaces GridHierarchy construction (grid_hierarchy.hpp:51-70, build_caches
  * :163-188) and the per-call workspace of correction_level (correction.hpp:301).
- * A plan is immutable after creation and may be shared by host threads that
- * use distinct streams only if they do not run concurrently on it (the
- * workspace is per plan); create one plan per stream for concurrency. */
+ * A plan may be shared by host threads and streams: calls on one plan are
+ * serialised (a per-plan lock while a call enqueues, and each call's work is
+ * ordered after the previous call's by an event), so results never depend on
+ * interleaving. For concurrent execution create one plan per stream; the
+ * one-shot entry points below do this themselves (a small pool of plans per
+ * grid, "distinct arrays may be processed concurrently"). */
 int hgr_cuda_plan_create(const hgr_grid_desc* grid, int dtype, hgr_plan* out);
 void hgr_cuda_plan_destroy(hgr_plan plan);
 /* GridHierarchy::levels() (grid_hierarchy.hpp:85) */
@@ -139,7 +142,10 @@ int hgr_cuda_recompose_f32(const hgr_grid_desc* grid, const float* d_in, float* 
 
 /* Host-pointer convenience (synchronous: H2D, run, D2H). This is what the
  * C++ template drop-in (include/hgr_b200/hgr.hpp) calls. decompose checks
- * finiteness before touching h_data (refactor.hpp:36-38). */
+ * finiteness before touching h_data (refactor.hpp:36-38). Device buffers are
+ * cached per plan; pinned host buffers move by direct DMA, pageable ones
+ * through a pinned staging ring with a multi-threaded host copy overlapping
+ * the DMA. Thread-safe (plan pool, as above). */
 int hgr_decompose_host_f64(const hgr_grid_desc* grid, double* h_data);
 int hgr_decompose_host_f32(const hgr_grid_desc* grid, float* h_data);
 int hgr_recompose_host_f64(const hgr_grid_desc* grid, const double* h_in, double* h_out,
@@ -166,6 +172,16 @@ int hgr_cuda_compute_correction_f64(const hgr_grid_desc* g, int level, const dou
 int hgr_cuda_compute_correction_f32(const hgr_grid_desc* g, int level, const float* d_coeffs,
                                     float* d_z, void* stream);
 
+/* apply_coefficients (transforms.hpp:115-124): fine = interpolate_to_fine(coarse) + coeffs */
+int hgr_cuda_apply_coefficients_f64(const hgr_grid_desc* g, int level, const double* d_coarse,
+                                    const double* d_coeffs, double* d_fine, void* stream);
+int hgr_cuda_apply_coefficients_f32(const hgr_grid_desc* g, int level, const float* d_coarse,
+                                    const float* d_coeffs, float* d_fine, void* stream);
+int hgr_host_apply_coefficients_f64(const hgr_grid_desc* g, int level, const double* h_coarse,
+                                    const double* h_coeffs, double* h_fine);
+int hgr_host_apply_coefficients_f32(const hgr_grid_desc* g, int level, const float* h_coarse,
+                                    const float* h_coeffs, float* h_fine);
+
 /* Host-pointer twins of the single-level entry points (synchronous), used by
  * the C++ drop-in: op 0 = interpolate_to_fine, 1 = compute_coefficients,
  * 2 = compute_correction. h_in / h_out are compact level arrays. */
@@ -173,8 +189,10 @@ int hgr_host_level_op_f64(const hgr_grid_desc* g, int op, int level, const doubl
                           double* h_out);
 int hgr_host_level_op_f32(const hgr_grid_desc* g, int op, int level, const float* h_in,
                           float* h_out);
-/* Host-pointer fiber operators: op 0 = mass_apply, 1 = masstrans_apply,
- * 2 = thomas_solve (correction.hpp:58-223); count fibers of length n. */
+/* Host-pointer fiber operators (correction.hpp:58-223); count fibers of
+ * length n: op 0 = mass_apply, 1 = masstrans_apply, 2 = thomas_solve,
+ * 3 = transfer_apply, 4 = MassTransOperator::apply_fiber with
+ * zero_even_inputs (even fine inputs read as 0, correction.hpp:147-150). */
 int hgr_host_fiber_op_f64(int op, size_t n, size_t count, const double* h_v, const double* h_h,
                           double* h_out);
 int hgr_host_fiber_op_f32(int op, size_t n, size_t count, const float* h_v, const float* h_h,
@@ -201,6 +219,13 @@ int hgr_levels(const hgr_grid_desc* g);
  * shared by all fibers. Outputs: mass n, transfer/masstrans (n-1)/2+1, thomas n. */
 int hgr_cuda_mass_apply_f64(size_t n, size_t count, const double* d_v, const double* h_h,
                             double* d_out, void* stream);
+int hgr_cuda_mass_apply_f32(size_t n, size_t count, const float* d_v, const float* h_h,
+                            float* d_out, void* stream);
+/* transfer_apply (correction.hpp:67-88): R = P^T, weights refined_node_weights<T> */
+int hgr_cuda_transfer_apply_f64(size_t n, size_t count, const double* d_v, const double* h_h,
+                                double* d_out, void* stream);
+int hgr_cuda_transfer_apply_f32(size_t n, size_t count, const float* d_v, const float* h_h,
+                                float* d_out, void* stream);
 int hgr_cuda_masstrans_apply_f64(size_t n, size_t count, const double* d_v, const double* h_h,
                                  double* d_out, void* stream);
 int hgr_cuda_thomas_solve_f64(size_t n, size_t count, const double* d_rhs, const double* h_h,
@@ -209,6 +234,31 @@ int hgr_cuda_masstrans_apply_f32(size_t n, size_t count, const float* d_v, const
                                  float* d_out, void* stream);
 int hgr_cuda_thomas_solve_f32(size_t n, size_t count, const float* d_rhs, const float* h_h,
                               float* d_out, void* stream);
+
+/* ---- operator tables (host) -------------------------------------------------
+ * The builders the plans use, in T and in the reference's arithmetic order:
+ * MassTransOperator<T> taps (correction.hpp:96-133), 5 per coarse row over fine
+ * 2i-2..2i+2, (n-1)/2+1 rows for n fine nodes; ThomasSolver<T> factors
+ * (correction.hpp:188-198): mult n-1, pivot n, upper n-1. h holds n-1 spacings. */
+int hgr_masstrans_taps_f64(size_t n, const double* h_h, double* h_taps);
+int hgr_masstrans_taps_f32(size_t n, const float* h_h, float* h_taps);
+int hgr_thomas_factors_f64(size_t n, const double* h_h, double* h_mult, double* h_pivot,
+                           double* h_upper);
+int hgr_thomas_factors_f32(size_t n, const float* h_h, float* h_mult, float* h_pivot,
+                           float* h_upper);
+
+/* ---- error_report (refactor.hpp:100-120) on the device ------------------------
+ * L2 / Linf absolute and relative errors of d_b against d_a (n values each),
+ * accumulated in double by a deterministic two-level reduction (no atomics, so
+ * run-to-run identical). out[4] = {l2_abs, l2_rel, linf_abs, linf_rel};
+ * synchronizes `stream`. */
+int hgr_cuda_error_report_f64(size_t n, const double* d_a, const double* d_b, double* h_out,
+                              void* stream);
+int hgr_cuda_error_report_f32(size_t n, const float* d_a, const float* d_b, double* h_out,
+                              void* stream);
+/* host-pointer twins (the C++ drop-in's error_report on host ndarrays) */
+int hgr_error_report_host_f64(size_t n, const double* h_a, const double* h_b, double* h_out);
+int hgr_error_report_host_f32(size_t n, const float* h_a, const float* h_b, double* h_out);
 
 /* ---- the progressive .hg container (storage.hpp:17-218) ----------------------
  * Files are byte-identical to hgr::write_file's. Classes are packed / unpacked
@@ -241,6 +291,16 @@ int hgr_cuda_read_hg_prefix_f64(const char* path, int upto_class, double* d_pyra
                                 uint64_t* bytes_read, void* stream);
 int hgr_cuda_read_hg_prefix_f32(const char* path, int upto_class, float* d_pyramid,
                                 uint64_t* bytes_read, void* stream);
+/* host-pointer twins (the C++ drop-in's write_file / read_prefix): the pyramid
+ * is staged through the plan's device buffer and packed / scattered there */
+int hgr_write_hg_host_f64(const char* path, const hgr_grid_desc* g, const double* h_pyramid,
+                          uint64_t* bytes_written);
+int hgr_write_hg_host_f32(const char* path, const hgr_grid_desc* g, const float* h_pyramid,
+                          uint64_t* bytes_written);
+int hgr_read_hg_prefix_host_f64(const char* path, int upto_class, double* h_pyramid,
+                                uint64_t* bytes_read);
+int hgr_read_hg_prefix_host_f32(const char* path, int upto_class, float* h_pyramid,
+                                uint64_t* bytes_read);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ error_report               error_report                        (refactor.hpp:100
 extract_class/scatter_class extract_class / scatter_class      (refactor.hpp:149-170)
 interpolate_to_fine, compute_coefficients, apply_coefficients (transforms.hpp:76-124)
 compute_correction         compute_correction                  (correction.hpp:348-365)
-masstrans_apply, thomas_solve, mass_apply (correction.hpp:58-223)
+masstrans_apply, thomas_solve, mass_apply, transfer_apply (correction.hpp:58-223)
 hgr::error                 HgrError (error.hpp:9-11)
 =========================  ==================================================
 
@@ -38,7 +38,7 @@ __all__ = [
     "HgrError", "GridHierarchy", "RefactoredArray", "Plan", "decompose", "recompose",
     "error_report", "ErrorReport", "extract_class", "scatter_class", "interpolate_to_fine",
     "compute_coefficients", "apply_coefficients", "compute_correction", "masstrans_apply",
-    "thomas_solve", "mass_apply", "build_hierarchy",
+    "thomas_solve", "mass_apply", "transfer_apply", "build_hierarchy",
 ]
 
 
@@ -196,7 +196,10 @@ class Plan:
     and dtype -- hgr_cuda_plan_* in the C ABI."""
 
     def __init__(self, g: GridHierarchy, dtype: str = "f64"):
+        if dtype not in ("f64", "f32"):
+            raise HgrError("dtype must be 'f32' or 'f64'")
         self.hierarchy = g
+        self.dtype = dtype
         self._h = C.c_void_p()
         _check(_lib.load().hgr_cuda_plan_create(C.byref(g.desc),
                                                  _lib.HGR_F64 if dtype == "f64" else _lib.HGR_F32,
@@ -222,17 +225,41 @@ class Plan:
     def launches(self, direction: int, upto_class: int) -> int:
         return _lib.load().hgr_cuda_plan_launches(self._h, direction, upto_class)
 
+    def _operand(self, x, what: str):
+        """A plan operand must be a contiguous CUDA tensor of the plan's finest
+        shape and dtype (the kernels trust these; a mismatch would read or
+        write past the tensor)."""
+        import torch
+        if not _is_torch(x) or not x.is_cuda:
+            raise HgrError(f"{what}: expected a CUDA tensor")
+        if list(x.shape) != self.hierarchy.finest_extents():
+            raise HgrError(f"{what}: array shape does not match grid")
+        if x.dtype != (torch.float64 if self.dtype == "f64" else torch.float32):
+            raise HgrError(f"{what}: dtype {x.dtype} does not match the plan ({self.dtype})")
+        if not x.is_contiguous():
+            raise HgrError(f"{what}: tensor must be contiguous")
+        return x
+
+    def _pair(self, src, out, what: str):
+        self._operand(src, what)
+        self._operand(out, what)
+        if src.device != out.device:
+            raise HgrError(f"{what}: input and output are on different devices")
+
     def decompose_(self, data, stream: Optional[int] = None) -> None:
         """In-place, stream-ordered decompose of a device tensor (no sync)."""
+        self._operand(data, "decompose")
         _check(_lib.load().hgr_cuda_plan_decompose(self._h, _ptr(data),
                                                    stream if stream is not None else _stream_of(data)))
 
     def decompose_into(self, src, out, stream: Optional[int] = None) -> None:
         """Out-of-place, stream-ordered decompose (src untouched; no sync)."""
+        self._pair(src, out, "decompose")
         _check(_lib.load().hgr_cuda_plan_decompose_to(self._h, _ptr(src), _ptr(out),
                                                       stream if stream is not None else _stream_of(src)))
 
     def recompose_into(self, src, out, upto_class: int, stream: Optional[int] = None) -> None:
+        self._pair(src, out, "recompose")
         _check(_lib.load().hgr_cuda_plan_recompose(self._h, _ptr(src), _ptr(out), int(upto_class),
                                                    stream if stream is not None else _stream_of(src)))
 
@@ -244,6 +271,7 @@ class Plan:
         fused decompose / recompose / interpolation kernels per level with the
         sector model (perf_model.hpp:71-137), time the top three, keep the
         fastest. src is read, out is overwritten. Returns the JSON report."""
+        self._pair(src, out, "autotune")
         lib = _lib.load()
         st = stream if stream is not None else _stream_of(src)
         n = C.c_size_t(0)
@@ -282,11 +310,16 @@ def decompose(data, g: GridHierarchy) -> RefactoredArray:
     _check_shape(data, g, "decompose")
     t = _dtype_tag(data)
     lib = _lib.load()
-    if _is_torch(data):
+    if _is_torch(data) and data.is_cuda:
         src = data.detach().contiguous()
         out = src.new_empty(src.shape)
         _check(getattr(lib, f"hgr_cuda_decompose_to_{t}")(C.byref(g.desc), _ptr(src), _ptr(out),
                                                            _stream_of(src)))
+    elif _is_torch(data):  # host tensor (pinned ones move by direct DMA)
+        import torch
+        out = torch.empty(tuple(data.shape), dtype=data.dtype, pin_memory=data.is_pinned())
+        out.copy_(data)
+        _check(getattr(lib, f"hgr_decompose_host_{t}")(C.byref(g.desc), _ptr(out)))
     else:
         out = np.array(data, copy=True, order="C")
         _check(getattr(lib, f"hgr_decompose_host_{t}")(C.byref(g.desc), _ptr(out)))
@@ -298,11 +331,16 @@ def recompose(r: RefactoredArray, upto_class: int):
     g, src = r.hierarchy, r.data
     t = _dtype_tag(src)
     lib = _lib.load()
-    if _is_torch(src):
+    if _is_torch(src) and src.is_cuda:
         src = src.contiguous()
         out = src.new_empty(src.shape)
         _check(getattr(lib, f"hgr_cuda_recompose_{t}")(C.byref(g.desc), _ptr(src), _ptr(out),
                                                         int(upto_class), _stream_of(src)))
+    elif _is_torch(src):  # host tensor
+        src = src.contiguous()
+        out = src.new_empty(src.shape, pin_memory=src.is_pinned())
+        _check(getattr(lib, f"hgr_recompose_host_{t}")(C.byref(g.desc), _ptr(src), _ptr(out),
+                                                        int(upto_class)))
     else:
         src = np.ascontiguousarray(src)
         out = np.empty_like(src)
@@ -320,30 +358,27 @@ class ErrorReport:
 
 
 def error_report(original, reconstruction) -> ErrorReport:
-    """error_report (refactor.hpp:100-120), accumulated in double."""
+    """error_report (refactor.hpp:100-120), accumulated in double by the
+    device reduction (hgr_cuda_error_report_*); host arrays are staged to the
+    current CUDA device."""
     if tuple(original.shape) != tuple(reconstruction.shape):
         raise HgrError("error_report: shape mismatch")
-    if _is_torch(original):
-        a = original.double()
-        d = a - reconstruction.double()
-        sq_diff, sq_orig = float((d * d).sum()), float((a * a).sum())
-        max_diff = float(d.abs().max()) if d.numel() else 0.0
-        max_orig = float(a.abs().max()) if a.numel() else 0.0
-    else:
-        a = np.asarray(original, dtype=np.float64)
-        d = a - np.asarray(reconstruction, dtype=np.float64)
-        sq_diff, sq_orig = float((d * d).sum()), float((a * a).sum())
-        max_diff, max_orig = float(np.abs(d).max()), float(np.abs(a).max())
-    rep = ErrorReport(l2_abs=sq_diff ** 0.5, linf_abs=max_diff)
-    inf = float("inf")
-    rep.l2_rel = rep.l2_abs / sq_orig ** 0.5 if sq_orig > 0 else (inf if rep.l2_abs > 0 else 0.0)
-    rep.linf_rel = rep.linf_abs / max_orig if max_orig > 0 else (inf if rep.linf_abs > 0 else 0.0)
-    return rep
+    if original.numel() if _is_torch(original) else np.size(original) == 0:
+        return ErrorReport()
+    a, _ = _to_device(original)
+    b, _ = _to_device(reconstruction)
+    if a.dtype != b.dtype:
+        b = b.to(a.dtype)
+    b = b.to(a.device).contiguous()
+    out = (C.c_double * 4)()
+    _check(getattr(_lib.load(), f"hgr_cuda_error_report_{_dtype_tag(a)}")(
+        a.numel(), _ptr(a), _ptr(b), out, _stream_of(a)))
+    return ErrorReport(l2_abs=out[0], l2_rel=out[1], linf_abs=out[2], linf_rel=out[3])
 
 
 def _to_device(x):
     if _is_torch(x):
-        return x.contiguous(), True
+        return (x.contiguous(), True) if x.is_cuda else (x.contiguous().cuda(), False)
     import torch
     return torch.from_numpy(np.ascontiguousarray(x)).cuda(), False
 
@@ -417,8 +452,14 @@ def apply_coefficients(coarse, coeffs, g: GridHierarchy, level: int):
     _require_level(g, level)
     if list(coarse.shape) != g.level_extents(level - 1) or list(coeffs.shape) != g.level_extents(level):
         raise HgrError("apply_coefficients: shape mismatch")
-    fine = interpolate_to_fine(coarse, g, level)
-    return fine + coeffs
+    import torch
+    c, was = _to_device(coarse)
+    k, _ = _to_device(coeffs)
+    k = k.to(device=c.device, dtype=c.dtype).contiguous()
+    out = torch.empty(g.level_extents(level), dtype=c.dtype, device=c.device)
+    _check(getattr(_lib.load(), f"hgr_cuda_apply_coefficients_{_dtype_tag(c)}")(
+        C.byref(g.desc), int(level), _ptr(c), _ptr(k), _ptr(out), _stream_of(c)))
+    return _back(out, was)
 
 
 def compute_correction(coeffs, g: GridHierarchy, level: int):
@@ -467,8 +508,16 @@ def synthetic_field(shape, dtype: str = "f64", seed: int = 12345, device=None):
 
 
 def mass_apply(v, h):
-    """mass_apply (correction.hpp:58-62), float64."""
+    """mass_apply (correction.hpp:58-62)."""
     return _fiber("mass_apply", v, h, lambda n: n)
+
+
+def transfer_apply(v, h):
+    """transfer_apply (correction.hpp:67-88): R = P^T on one fiber (or a batch)."""
+    n = v.shape[-1]
+    if n < 3 or n % 2 == 0:
+        raise HgrError("transfer_apply: fine fiber length must be odd")
+    return _fiber("transfer_apply", v, h, lambda n: (n - 1) // 2 + 1)
 
 
 def masstrans_apply(v, h):

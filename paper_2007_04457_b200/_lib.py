@@ -70,12 +70,23 @@ for _t in ("f64", "f32"):
         f"hgr_cuda_extract_class_{_t}": (_int, [_G, _vp, _int, _vp, _vp]),
         f"hgr_cuda_scatter_class_{_t}": (_int, [_G, _vp, _int, _vp, _vp]),
         f"hgr_cuda_masstrans_apply_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
+        f"hgr_cuda_mass_apply_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
+        f"hgr_cuda_transfer_apply_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
+        f"hgr_cuda_error_report_{_t}": (_int, [_sz, _vp, _vp, _vp, _vp]),
+        f"hgr_masstrans_taps_{_t}": (_int, [_sz, _vp, _vp]),
+        f"hgr_thomas_factors_{_t}": (_int, [_sz, _vp, _vp, _vp, _vp]),
+        f"hgr_host_level_op_{_t}": (_int, [_G, _int, _int, _vp, _vp]),
+        f"hgr_host_fiber_op_{_t}": (_int, [_int, _sz, _sz, _vp, _vp, _vp]),
+        f"hgr_cuda_apply_coefficients_{_t}": (_int, [_G, _int, _vp, _vp, _vp, _vp]),
+        f"hgr_host_apply_coefficients_{_t}": (_int, [_G, _int, _vp, _vp, _vp]),
+        f"hgr_error_report_host_{_t}": (_int, [_sz, _vp, _vp, _vp]),
+        f"hgr_write_hg_host_{_t}": (_int, [C.c_char_p, _G, _vp, C.POINTER(C.c_uint64)]),
+        f"hgr_read_hg_prefix_host_{_t}": (_int, [C.c_char_p, _int, _vp, C.POINTER(C.c_uint64)]),
         f"hgr_cuda_thomas_solve_{_t}": (_int, [_sz, _sz, _vp, _vp, _vp, _vp]),
         f"hgr_cuda_write_hg_{_t}": (_int, [C.c_char_p, _G, _vp, C.POINTER(C.c_uint64), _vp]),
         f"hgr_cuda_read_hg_prefix_{_t}": (_int, [C.c_char_p, _int, _vp, C.POINTER(C.c_uint64),
                                                    _vp]),
     })
-_SIGS["hgr_cuda_mass_apply_f64"] = (_int, [_sz, _sz, _vp, _vp, _vp, _vp])
 
 EXPORTED_SYMBOLS = tuple(sorted(_SIGS))
 

@@ -11,6 +11,8 @@
 #include "../../include/hgr_cuda.h"
 #include "kernels.cuh"
 #include "plan.hpp"
+#include "hostio.hpp"
+#include "tables.hpp"
 #include "storage.hpp"
 
 using hgrb::Error;
@@ -69,30 +71,93 @@ CacheKey make_key(const hgr_grid_desc* g, int dtype) {
   return k;
 }
 
+// Each grid key holds a small pool of plans: a call leases one that no other
+// host thread is using (a second plan is built when all are busy, up to
+// kPoolCap), so distinct arrays of the same grid are processed concurrently
+// (SPEC.md:287); a lease also orders the call's stream after the previous
+// user of that plan (Plan::begin_use / end_use).
+struct CacheEntry {
+  CacheKey key;
+  std::vector<std::shared_ptr<Plan>> pool;
+};
 std::mutex g_cache_mu;
-std::list<std::pair<CacheKey, std::shared_ptr<Plan>>> g_cache;  // MRU first
+std::list<CacheEntry> g_cache;  // MRU first
 constexpr std::size_t kCacheCap = 8;
+constexpr std::size_t kPoolCap = 4;
 
-std::shared_ptr<Plan> cached_plan(const hgr_grid_desc* g, int dtype) {
+// kHostCall: the caller orders its work on the plan's private host stream itself
+const cudaStream_t kHostCall = reinterpret_cast<cudaStream_t>(~uintptr_t(0));
+
+struct Lease {
+  std::shared_ptr<Plan> plan;
+  std::unique_lock<std::recursive_mutex> lock;
+  cudaStream_t s;
+  Lease(std::shared_ptr<Plan> p, std::unique_lock<std::recursive_mutex> l, cudaStream_t st)
+      : plan(std::move(p)), lock(std::move(l)), s(st) {
+    if (s != kHostCall) plan->begin_use(s);
+  }
+  Lease(Lease&&) = default;
+  ~Lease() {
+    if (plan && lock.owns_lock() && s != kHostCall) plan->end_use(s);
+  }
+  Plan* operator->() const { return plan.get(); }
+  Plan& operator*() const { return *plan; }
+};
+
+Lease cached_plan(const hgr_grid_desc* g, int dtype, cudaStream_t s = nullptr) {
   CacheKey key = make_key(g, dtype);
-  std::lock_guard<std::mutex> lock(g_cache_mu);
-  for (auto it = g_cache.begin(); it != g_cache.end(); ++it)
-    if (it->first == key) {
+  std::shared_ptr<Plan> busy;
+  {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    auto it = g_cache.begin();
+    for (; it != g_cache.end(); ++it)
+      if (it->key == key) break;
+    if (it != g_cache.end()) {
       g_cache.splice(g_cache.begin(), g_cache, it);
-      return g_cache.front().second;
+      for (auto& p : g_cache.front().pool) {
+        std::unique_lock<std::recursive_mutex> l(p->use_mu, std::try_to_lock);
+        if (l.owns_lock()) return Lease(p, std::move(l), s);
+      }
+      if (g_cache.front().pool.size() >= kPoolCap) busy = g_cache.front().pool.front();
     }
+  }
+  if (busy) {  // every plan of the pool is in use: wait for the first
+    std::unique_lock<std::recursive_mutex> l(busy->use_mu);
+    return Lease(busy, std::move(l), s);
+  }
+  // build outside the cache lock (uploads tables, allocates the workspace)
   std::shared_ptr<Plan> p(hgrb::make_plan(g, dtype).release());
-  g_cache.emplace_front(std::move(key), p);
-  if (g_cache.size() > kCacheCap) g_cache.pop_back();
-  return p;
+  std::unique_lock<std::recursive_mutex> l(p->use_mu);
+  {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    auto it = g_cache.begin();
+    for (; it != g_cache.end(); ++it)
+      if (it->key == key) break;
+    if (it == g_cache.end()) {
+      g_cache.push_front(CacheEntry{std::move(key), {}});
+      it = g_cache.begin();
+      if (g_cache.size() > kCacheCap) g_cache.pop_back();
+    }
+    if (it->pool.size() < kPoolCap) it->pool.push_back(p);
+  }
+  return Lease(p, std::move(l), s);
 }
+
+// an explicit plan handle: same serialisation, no pool
+struct PlanUse {
+  Plan& p;
+  cudaStream_t s;
+  std::lock_guard<std::recursive_mutex> lock;
+  PlanUse(Plan& pl, cudaStream_t st) : p(pl), s(st), lock(pl.use_mu) { p.begin_use(s); }
+  ~PlanUse() { p.end_use(s); }
+};
 
 std::size_t finest_count(const Plan& p) { return p.h.node_count(p.h.L); }
 
 template <class T>
 int decompose_dev(const hgr_grid_desc* g, T* d, void* stream) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, as_stream(stream));
     p->decompose(d, as_stream(stream));
     int st = p->sync_status(as_stream(stream));
     if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
@@ -102,7 +167,7 @@ int decompose_dev(const hgr_grid_desc* g, T* d, void* stream) {
 template <class T>
 int decompose_to_dev(const hgr_grid_desc* g, const T* in, T* out, void* stream) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, as_stream(stream));
     p->decompose_to(in, out, as_stream(stream));
     int st = p->sync_status(as_stream(stream));
     if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
@@ -112,7 +177,7 @@ int decompose_to_dev(const hgr_grid_desc* g, const T* in, T* out, void* stream) 
 template <class T>
 int recompose_dev(const hgr_grid_desc* g, const T* in, T* out, int m, void* stream) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, as_stream(stream));
     p->recompose(in, out, m, as_stream(stream));
   });
 }
@@ -124,39 +189,50 @@ struct DevBuf {
   ~DevBuf() { cudaFree(p); }
 };
 
+// Host-pointer decompose / recompose (the reference's ndarray calls,
+// refactor.hpp:32-33, :63-68): the plan's cached device buffers and private
+// stream, pinned sources by direct DMA, pageable ones through the staging ring
+// (hostio.cu). Synchronous like the reference.
 template <class T>
 int decompose_host(const hgr_grid_desc* g, T* h) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
-    const std::size_t n = finest_count(*p);
-    DevBuf<T> d(n), o(n);
-    cudaStream_t s = nullptr;
-    HGR_CUDA_CHECK(cudaMemcpy(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, kHostCall);
+    cudaStream_t s = hgrb::host_stream(*p);
+    p->begin_use(s);
+    const std::size_t bytes = finest_count(*p) * sizeof(T);
+    void* din = hgrb::host_device_buffer(*p, 0, bytes);
+    void* dout = hgrb::host_device_buffer(*p, 1, bytes);
+    hgrb::host_to_device(*p, din, h, bytes, s);
+    p->decompose_to(din, dout, s);
     // finiteness is validated before h is modified (refactor.hpp:36-38)
-    p->decompose_to(d.p, o.p, s);
-    int st = p->sync_status(s);
+    const int st = p->sync_status(s);
     if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
-    HGR_CUDA_CHECK(cudaMemcpy(h, o.p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    hgrb::device_to_host(*p, h, dout, bytes, s);
+    p->end_use(s);
   });
 }
 
 template <class T>
 int recompose_host(const hgr_grid_desc* g, const T* in, T* out, int m) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
-    const std::size_t n = finest_count(*p);
-    DevBuf<T> d(n);
-    HGR_CUDA_CHECK(cudaMemcpy(d.p, in, n * sizeof(T), cudaMemcpyHostToDevice));
-    p->recompose(d.p, d.p, m, nullptr);
-    HGR_CUDA_CHECK(cudaMemcpy(out, d.p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, kHostCall);
+    cudaStream_t s = hgrb::host_stream(*p);
+    p->begin_use(s);
+    const std::size_t bytes = finest_count(*p) * sizeof(T);
+    void* din = hgrb::host_device_buffer(*p, 0, bytes);
+    void* dout = hgrb::host_device_buffer(*p, 1, bytes);
+    hgrb::host_to_device(*p, din, in, bytes, s);
+    p->recompose(din, dout, m, s);
+    hgrb::device_to_host(*p, out, dout, bytes, s);
+    p->end_use(s);
   });
 }
 
 template <class T>
 int single_level(const hgr_grid_desc* g, int op, int level, const T* in, T* out, void* stream) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
     cudaStream_t s = as_stream(stream);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, s);
     if (op == 0) p->interpolate_to_fine(level, in, out, s);
     else if (op == 1) p->compute_coefficients(level, in, out, s);
     else p->compute_correction(level, in, out, s);
@@ -167,52 +243,13 @@ int single_level(const hgr_grid_desc* g, int op, int level, const T* in, T* out,
 template <class T>
 int class_copy(const hgr_grid_desc* g, T* data, int cls, T* vals, bool extract, void* stream) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, as_stream(stream));
     p->class_copy(data, cls, vals, extract, as_stream(stream));
     HGR_CUDA_CHECK(cudaStreamSynchronize(as_stream(stream)));
   });
 }
 
 // ---- fiber operators ------------------------------------------------------------
-
-template <class T>
-std::vector<T> fiber_taps(std::size_t n, const T* h) {
-  hgrb::require(n >= 3 && (n - 1) % 2 == 0, "mass-trans: fine fiber length must be odd");
-  const std::size_t nf = n, nc = (nf - 1) / 2 + 1;
-  std::vector<T> taps(nc * 5, T(0));
-  auto main_ = [&](std::size_t i) {
-    const T left = i > 0 ? h[i - 1] : T(0);
-    const T right = i + 1 < nf ? h[i] : T(0);
-    return T(2) * (left + right);
-  };
-  for (std::size_t i = 0; i < nc; ++i) {
-    std::size_t rj[3];
-    T rw[3];
-    std::size_t rn = 0;
-    if (i > 0) {
-      rj[rn] = 2 * i - 1;
-      rw[rn++] = h[2 * i - 2] / (h[2 * i - 2] + h[2 * i - 1]);
-    }
-    rj[rn] = 2 * i;
-    rw[rn++] = T(1);
-    if (i + 1 < nc) {
-      rj[rn] = 2 * i + 1;
-      rw[rn++] = h[2 * i + 1] / (h[2 * i] + h[2 * i + 1]);
-    }
-    for (std::size_t k = 0; k < 5; ++k) {
-      const long j = long(2 * i) - 2 + long(k);
-      if (j < 0 || j >= long(nf)) continue;
-      T sum = T(0);
-      for (std::size_t r = 0; r < rn; ++r) {
-        const std::size_t t = rj[r], jj = std::size_t(j);
-        const T me = jj == t ? main_(t) : (jj + 1 == t ? h[t - 1] : (jj == t + 1 ? h[t] : T(0)));
-        sum += rw[r] * me;
-      }
-      taps[i * 5 + k] = sum;
-    }
-  }
-  return taps;
-}
 
 template <class T>
 T* upload(const std::vector<T>& v, std::vector<void*>& owned) {
@@ -230,33 +267,34 @@ struct Owned {
   }
 };
 
+// op: 0 mass_apply, 1 masstrans_apply, 2 thomas_solve, 3 transfer_apply,
+// 4 masstrans with even inputs masked (MassTransOperator::apply_fiber's
+// zero_even_inputs). Tables come from the plan's builders (tables.hpp).
 template <class T>
 int fiber_op(int op, std::size_t n, std::size_t count, const T* v, const T* h, T* out,
              void* stream) {
   return guarded([&] {
     hgrb::require(n >= 2, "mass matrix needs at least one interval");
+    if (op == 1 || op == 3 || op == 4)
+      hgrb::require(n >= 3 && (n - 1) % 2 == 0,
+                    op == 3 ? "transfer_apply: fine fiber length must be odd"
+                            : "mass-trans: fine fiber length must be odd");
     cudaStream_t s = as_stream(stream);
     Owned own;
     std::vector<T> hv(h, h + n - 1);
     if (op == 0) {
       hgrb::launch_fiber_mass<T>(v, out, int64_t(n), int64_t(count), upload(hv, own.p), s);
-    } else if (op == 1) {
+    } else if (op == 1 || op == 4) {
       hgrb::launch_fiber_masstrans<T>(v, out, int64_t(n), int64_t(count),
-                                      upload(fiber_taps<T>(n, h), own.p), s);
+                                      upload(hgrb::masstrans_taps<T>(hv), own.p), op == 4, s);
+    } else if (op == 3) {
+      std::vector<T> trl, trr;
+      hgrb::transfer_weights<T>(hv, trl, trr);
+      hgrb::launch_fiber_transfer<T>(v, out, int64_t(n), int64_t(count), upload(trl, own.p),
+                                     upload(trr, own.p), s);
     } else {
-      std::vector<T> mult(n - 1), pivot(n), upper(n - 1), rpiv(n);
-      auto main_ = [&](std::size_t i) {
-        const T left = i > 0 ? h[i - 1] : T(0);
-        const T right = i + 1 < n ? h[i] : T(0);
-        return T(2) * (left + right);
-      };
-      for (std::size_t i = 0; i < n; ++i) pivot[i] = main_(i);
-      for (std::size_t i = 0; i + 1 < n; ++i) upper[i] = h[i];
-      for (std::size_t i = 1; i < n; ++i) {
-        mult[i - 1] = h[i - 1] / pivot[i - 1];
-        pivot[i] = main_(i) - mult[i - 1] * upper[i - 1];
-      }
-      for (std::size_t i = 0; i < n; ++i) rpiv[i] = T(1) / pivot[i];
+      std::vector<T> mult, pivot, upper, rpiv;
+      hgrb::thomas_factors<T>(hv, mult, pivot, upper, rpiv);
       hgrb::launch_fiber_thomas<T>(v, out, int64_t(n), int64_t(count), upload(mult, own.p),
                                    upload(rpiv, own.p), upload(upper, own.p), s);
     }
@@ -267,23 +305,111 @@ int fiber_op(int op, std::size_t n, std::size_t count, const T* v, const T* h, T
 template <class T>
 int host_level_op(const hgr_grid_desc* g, int op, int level, const T* h_in, T* h_out) {
   return guarded([&] {
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, kHostCall);
     hgrb::require(level >= 1 && level <= p->h.L, "level out of range");
     const std::size_t nf = p->h.node_count(level), nc = p->h.node_count(level - 1);
     const std::size_t nin = op == 0 ? nc : nf, nout = op == 2 ? nc : nf;
-    DevBuf<T> din(nin), dout(nout);
-    HGR_CUDA_CHECK(cudaMemcpy(din.p, h_in, nin * sizeof(T), cudaMemcpyHostToDevice));
+    cudaStream_t s = hgrb::host_stream(*p);
+    p->begin_use(s);
+    void* din = hgrb::host_device_buffer(*p, 0, nin * sizeof(T));
+    void* dout = hgrb::host_device_buffer(*p, 1, nout * sizeof(T));
+    hgrb::host_to_device(*p, din, h_in, nin * sizeof(T), s);
+    if (op == 0) p->interpolate_to_fine(level, din, dout, s);
+    else if (op == 1) p->compute_coefficients(level, din, dout, s);
+    else p->compute_correction(level, din, dout, s);
+    hgrb::device_to_host(*p, h_out, dout, nout * sizeof(T), s);
+    p->end_use(s);
+  });
+}
+
+template <class T>
+int apply_coefficients_dev(const hgr_grid_desc* g, int level, const T* coarse, const T* coeffs,
+                           T* fine, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = as_stream(stream);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, s);
+    p->apply_coefficients(level, coarse, coeffs, fine, s);
+    HGR_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+template <class T>
+int apply_coefficients_host(const hgr_grid_desc* g, int level, const T* h_coarse,
+                            const T* h_coeffs, T* h_fine) {
+  return guarded([&] {
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, kHostCall);
+    hgrb::require(level >= 1 && level <= p->h.L, "level out of range");
+    const std::size_t nf = p->h.node_count(level), nc = p->h.node_count(level - 1);
+    cudaStream_t s = hgrb::host_stream(*p);
+    p->begin_use(s);
+    DevBuf<T> dc(nc), dcoef(nf);
+    T* df = static_cast<T*>(hgrb::host_device_buffer(*p, 1, nf * sizeof(T)));
+    hgrb::host_to_device(*p, dc.p, h_coarse, nc * sizeof(T), s);
+    hgrb::host_to_device(*p, dcoef.p, h_coeffs, nf * sizeof(T), s);
+    p->apply_coefficients(level, dc.p, dcoef.p, df, s);
+    hgrb::device_to_host(*p, h_fine, df, nf * sizeof(T), s);
+    p->end_use(s);
+  });
+}
+
+template <class T>
+int error_report_host(size_t n, const T* a, const T* b, double* out) {
+  return guarded([&] {
     cudaStream_t s = nullptr;
-    if (op == 0) p->interpolate_to_fine(level, din.p, dout.p, s);
-    else if (op == 1) p->compute_coefficients(level, din.p, dout.p, s);
-    else p->compute_correction(level, din.p, dout.p, s);
-    HGR_CUDA_CHECK(cudaMemcpy(h_out, dout.p, nout * sizeof(T), cudaMemcpyDeviceToHost));
+    HGR_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct S {
+      cudaStream_t s;
+      ~S() { cudaStreamDestroy(s); }
+    } guard{s};
+    DevBuf<T> da(n), db(n);
+    HGR_CUDA_CHECK(cudaMemcpyAsync(da.p, a, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    HGR_CUDA_CHECK(cudaMemcpyAsync(db.p, b, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    hgrb::error_report<T>(da.p, db.p, int64_t(n), out, s);
+  });
+}
+
+template <class T>
+int write_hg_host(const char* path, const hgr_grid_desc* g, const T* h, uint64_t* bytes) {
+  return guarded([&] {
+    hgrb::require(path != nullptr, "path is null");
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, kHostCall);
+    cudaStream_t s = hgrb::host_stream(*p);
+    p->begin_use(s);
+    const std::size_t nb = finest_count(*p) * sizeof(T);
+    void* d = hgrb::host_device_buffer(*p, 0, nb);
+    hgrb::host_to_device(*p, d, h, nb, s);
+    const uint64_t n = hgrb::hg_write(path, *p, d, s);
+    if (bytes) *bytes = n;
+    p->end_use(s);
+  });
+}
+
+template <class T>
+int read_hg_prefix_host(const char* path, int upto, T* h, uint64_t* bytes) {
+  return guarded([&] {
+    hgrb::require(path != nullptr, "path is null");
+    const hgrb::HgInfo info = hgrb::hg_read_info(path);
+    hgr_grid_desc g{};
+    g.rank = info.rank;
+    for (int k = 0; k < info.rank; ++k) {
+      g.extents[k] = info.extents[std::size_t(k)];
+      g.coords[k] = info.coords[std::size_t(k)].data();
+    }
+    auto p = cached_plan(&g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, kHostCall);
+    cudaStream_t s = hgrb::host_stream(*p);
+    p->begin_use(s);
+    const std::size_t nb = finest_count(*p) * sizeof(T);
+    void* d = hgrb::host_device_buffer(*p, 0, nb);
+    const uint64_t n = hgrb::hg_read_prefix(path, info, *p, upto, d, s);
+    hgrb::device_to_host(*p, h, d, nb, s);
+    if (bytes) *bytes = n;
+    p->end_use(s);
   });
 }
 
 template <class T>
 int host_fiber_op(int op, std::size_t n, std::size_t count, const T* h_v, const T* h_h, T* h_out) {
-  const std::size_t nout = op == 1 ? (n - 1) / 2 + 1 : n;
+  const std::size_t nout = (op == 1 || op == 3 || op == 4) ? (n - 1) / 2 + 1 : n;
   int rc = HGR_OK;
   rc = guarded([&] {
     hgrb::require(n >= 2, "mass matrix needs at least one interval");
@@ -294,6 +420,27 @@ int host_fiber_op(int op, std::size_t n, std::size_t count, const T* h_v, const 
     HGR_CUDA_CHECK(cudaMemcpy(h_out, dout.p, nout * count * sizeof(T), cudaMemcpyDeviceToHost));
   });
   return rc;
+}
+
+template <class T>
+int masstrans_taps_host(size_t n, const T* h, T* taps) {
+  return guarded([&] {
+    hgrb::require(h && taps, "null argument");
+    hgrb::require(n >= 3 && (n - 1) % 2 == 0, "mass-trans: fine fiber length must be odd");
+    const auto t = hgrb::masstrans_taps<T>(std::vector<T>(h, h + n - 1));
+    std::copy(t.begin(), t.end(), taps);
+  });
+}
+template <class T>
+int thomas_factors_host(size_t n, const T* h, T* mult, T* pivot, T* upper) {
+  return guarded([&] {
+    hgrb::require(n >= 2, "mass matrix needs at least one interval");
+    std::vector<T> m, p, u, r;
+    hgrb::thomas_factors<T>(std::vector<T>(h, h + n - 1), m, p, u, r);
+    if (mult) std::copy(m.begin(), m.begin() + std::ptrdiff_t(n - 1), mult);
+    if (pivot) std::copy(p.begin(), p.end(), pivot);
+    if (upper) std::copy(u.begin(), u.begin() + std::ptrdiff_t(n - 1), upper);
+  });
 }
 
 }  // namespace
@@ -345,6 +492,7 @@ int hgr_cuda_plan_launches(hgr_plan plan, int direction, int upto_class) {
 int hgr_cuda_plan_decompose(hgr_plan plan, void* d_data, void* stream) {
   return guarded([&] {
     hgrb::require(plan != nullptr, "plan is null");
+    PlanUse use(*plan->plan, as_stream(stream));
     plan->plan->decompose(d_data, as_stream(stream));
   });
 }
@@ -352,6 +500,7 @@ int hgr_cuda_plan_decompose(hgr_plan plan, void* d_data, void* stream) {
 int hgr_cuda_plan_decompose_to(hgr_plan plan, const void* d_in, void* d_out, void* stream) {
   return guarded([&] {
     hgrb::require(plan != nullptr, "plan is null");
+    PlanUse use(*plan->plan, as_stream(stream));
     plan->plan->decompose_to(d_in, d_out, as_stream(stream));
   });
 }
@@ -360,6 +509,7 @@ int hgr_cuda_plan_recompose(hgr_plan plan, const void* d_in, void* d_out, int up
                             void* stream) {
   return guarded([&] {
     hgrb::require(plan != nullptr, "plan is null");
+    PlanUse use(*plan->plan, as_stream(stream));
     plan->plan->recompose(d_in, d_out, upto_class, as_stream(stream));
   });
 }
@@ -368,6 +518,7 @@ int hgr_cuda_plan_sync_status(hgr_plan plan, void* stream) {
   int st = HGR_OK;
   int rc = guarded([&] {
     hgrb::require(plan != nullptr, "plan is null");
+    PlanUse use(*plan->plan, as_stream(stream));
     st = plan->plan->sync_status(as_stream(stream));
     if (st != HGR_OK) throw Error(st, "decompose: input contains non-finite values");
   });
@@ -379,6 +530,7 @@ int hgr_cuda_plan_autotune(hgr_plan plan, const void* d_in, void* d_out, void* s
   return guarded([&] {
     hgrb::require(plan != nullptr, "plan is null");
     hgrb::require(d_in != nullptr && d_out != nullptr, "autotune: null operand");
+    PlanUse use(*plan->plan, as_stream(stream));
     const std::string rep = plan->plan->autotune(d_in, d_out, as_stream(stream));
     if (report_len) *report_len = rep.size();
     if (report && report_bytes) {
@@ -502,11 +654,71 @@ int hgr_cuda_masstrans_apply_f64(size_t n, size_t c, const double* v, const doub
 int hgr_cuda_thomas_solve_f64(size_t n, size_t c, const double* v, const double* h, double* o, void* s) {
   return fiber_op(2, n, c, v, h, o, s);
 }
+int hgr_cuda_mass_apply_f32(size_t n, size_t c, const float* v, const float* h, float* o, void* s) {
+  return fiber_op(0, n, c, v, h, o, s);
+}
+int hgr_cuda_transfer_apply_f64(size_t n, size_t c, const double* v, const double* h, double* o, void* s) {
+  return fiber_op(3, n, c, v, h, o, s);
+}
+int hgr_cuda_transfer_apply_f32(size_t n, size_t c, const float* v, const float* h, float* o, void* s) {
+  return fiber_op(3, n, c, v, h, o, s);
+}
 int hgr_cuda_masstrans_apply_f32(size_t n, size_t c, const float* v, const float* h, float* o, void* s) {
   return fiber_op(1, n, c, v, h, o, s);
 }
 int hgr_cuda_thomas_solve_f32(size_t n, size_t c, const float* v, const float* h, float* o, void* s) {
   return fiber_op(2, n, c, v, h, o, s);
+}
+
+int hgr_masstrans_taps_f64(size_t n, const double* h, double* t) { return masstrans_taps_host(n, h, t); }
+int hgr_masstrans_taps_f32(size_t n, const float* h, float* t) { return masstrans_taps_host(n, h, t); }
+int hgr_thomas_factors_f64(size_t n, const double* h, double* m, double* p, double* u) {
+  return thomas_factors_host(n, h, m, p, u);
+}
+int hgr_thomas_factors_f32(size_t n, const float* h, float* m, float* p, float* u) {
+  return thomas_factors_host(n, h, m, p, u);
+}
+
+int hgr_cuda_apply_coefficients_f64(const hgr_grid_desc* g, int l, const double* c, const double* k,
+                                    double* f, void* s) {
+  return apply_coefficients_dev(g, l, c, k, f, s);
+}
+int hgr_cuda_apply_coefficients_f32(const hgr_grid_desc* g, int l, const float* c, const float* k,
+                                    float* f, void* s) {
+  return apply_coefficients_dev(g, l, c, k, f, s);
+}
+int hgr_host_apply_coefficients_f64(const hgr_grid_desc* g, int l, const double* c, const double* k,
+                                    double* f) {
+  return apply_coefficients_host(g, l, c, k, f);
+}
+int hgr_host_apply_coefficients_f32(const hgr_grid_desc* g, int l, const float* c, const float* k,
+                                    float* f) {
+  return apply_coefficients_host(g, l, c, k, f);
+}
+int hgr_error_report_host_f64(size_t n, const double* a, const double* b, double* o) {
+  return error_report_host(n, a, b, o);
+}
+int hgr_error_report_host_f32(size_t n, const float* a, const float* b, double* o) {
+  return error_report_host(n, a, b, o);
+}
+int hgr_write_hg_host_f64(const char* path, const hgr_grid_desc* g, const double* h, uint64_t* b) {
+  return write_hg_host(path, g, h, b);
+}
+int hgr_write_hg_host_f32(const char* path, const hgr_grid_desc* g, const float* h, uint64_t* b) {
+  return write_hg_host(path, g, h, b);
+}
+int hgr_read_hg_prefix_host_f64(const char* path, int upto, double* h, uint64_t* b) {
+  return read_hg_prefix_host(path, upto, h, b);
+}
+int hgr_read_hg_prefix_host_f32(const char* path, int upto, float* h, uint64_t* b) {
+  return read_hg_prefix_host(path, upto, h, b);
+}
+
+int hgr_cuda_error_report_f64(size_t n, const double* a, const double* b, double* o, void* s) {
+  return guarded([&] { hgrb::error_report<double>(a, b, int64_t(n), o, as_stream(s)); });
+}
+int hgr_cuda_error_report_f32(size_t n, const float* a, const float* b, double* o, void* s) {
+  return guarded([&] { hgrb::error_report<float>(a, b, int64_t(n), o, as_stream(s)); });
 }
 
 }  // extern "C"
@@ -519,7 +731,7 @@ template <class T>
 int write_hg(const char* path, const hgr_grid_desc* g, const T* d, uint64_t* bytes, void* s) {
   return guarded([&] {
     hgrb::require(path != nullptr, "path is null");
-    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, as_stream(s));
     const uint64_t n = hgrb::hg_write(path, *p, d, as_stream(s));
     if (bytes) *bytes = n;
   });
@@ -536,7 +748,7 @@ int read_hg_prefix(const char* path, int upto, T* d, uint64_t* bytes, void* s) {
       g.extents[k] = info.extents[std::size_t(k)];
       g.coords[k] = info.coords[std::size_t(k)].data();
     }
-    auto p = cached_plan(&g, sizeof(T) == 8 ? HGR_F64 : HGR_F32);
+    auto p = cached_plan(&g, sizeof(T) == 8 ? HGR_F64 : HGR_F32, as_stream(s));
     const uint64_t n = hgrb::hg_read_prefix(path, info, *p, upto, d, as_stream(s));
     if (bytes) *bytes = n;
   });

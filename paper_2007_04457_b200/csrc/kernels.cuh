@@ -136,12 +136,15 @@ void launch_class_copy(T* data, const int64_t finest_ext[3], int64_t stride,
 template <class T>
 void check_finite(const T* v, int64_t n, int* flag, cudaStream_t s);
 
-// fiber operators (correction.hpp:43-62, 141-154, 202-208), batched
+// fiber operators (correction.hpp:43-88, 141-154, 202-208), batched
 template <class T>
 void launch_fiber_mass(const T* v, T* out, int64_t n, int64_t count, const T* h, cudaStream_t s);
 template <class T>
 void launch_fiber_masstrans(const T* v, T* out, int64_t n, int64_t count, const T* taps,
-                            cudaStream_t s);
+                            bool zero_even, cudaStream_t s);
+template <class T>
+void launch_fiber_transfer(const T* v, T* out, int64_t n, int64_t count, const T* trl,
+                           const T* trr, cudaStream_t s);
 template <class T>
 void launch_fiber_thomas(const T* v, T* out, int64_t n, int64_t count, const T* mult,
                          const T* rpiv, const T* upper, cudaStream_t s);

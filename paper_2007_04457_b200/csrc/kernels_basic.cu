@@ -295,18 +295,37 @@ __global__ void k_fiber_mass(const T* __restrict__ v, T* __restrict__ out, int64
   }
 }
 
+// apply_fiber (correction.hpp:141-154); zero_even: even fine inputs read as 0
 template <class T>
 __global__ void k_fiber_masstrans(const T* __restrict__ v, T* __restrict__ out, int64_t n,
-                                  int64_t count, const T* __restrict__ taps) {
+                                  int64_t count, const T* __restrict__ taps, bool zero_even) {
   const int64_t nc = (n - 1) / 2 + 1;
   GRID_STRIDE(idx, nc * count) {
     const int64_t i = idx % nc, f = idx / nc;
     T acc = T(0);
     for (int k = 0; k < 5; ++k) {
       const int64_t j = 2 * i - 2 + k;
-      if (j < 0 || j >= n) continue;
+      if (j < 0 || j >= n || (zero_even && !(j & 1))) continue;
       acc += taps[i * 5 + k] * v[f * n + j];
     }
+    out[idx] = acc;
+  }
+}
+
+// transfer_apply (correction.hpp:67-88): coarse i gathers fine 2i with the
+// refined neighbours 2i-1 / 2i+1 at their interpolation weights toward i
+template <class T>
+__global__ void k_fiber_transfer(const T* __restrict__ v, T* __restrict__ out, int64_t n,
+                                 int64_t count, const T* __restrict__ trl,
+                                 const T* __restrict__ trr) {
+  const int64_t nc = (n - 1) / 2 + 1;
+  GRID_STRIDE(idx, nc * count) {
+    const int64_t i = idx % nc;
+    const T* f = v + (idx / nc) * n;
+    T acc = T(0);
+    if (i > 0) acc += trl[i] * f[2 * i - 1];
+    acc += f[2 * i];
+    if (i + 1 < nc) acc += trr[i] * f[2 * i + 1];
     out[idx] = acc;
   }
 }
@@ -416,8 +435,14 @@ void launch_fiber_mass(const T* v, T* out, int64_t n, int64_t count, const T* h,
 }
 template <class T>
 void launch_fiber_masstrans(const T* v, T* out, int64_t n, int64_t count, const T* taps,
-                            cudaStream_t s) {
-  LAUNCH(k_fiber_masstrans<T>, ((n - 1) / 2 + 1) * count, 256, s, v, out, n, count, taps);
+                            bool zero_even, cudaStream_t s) {
+  LAUNCH(k_fiber_masstrans<T>, ((n - 1) / 2 + 1) * count, 256, s, v, out, n, count, taps,
+         zero_even);
+}
+template <class T>
+void launch_fiber_transfer(const T* v, T* out, int64_t n, int64_t count, const T* trl,
+                           const T* trr, cudaStream_t s) {
+  LAUNCH(k_fiber_transfer<T>, ((n - 1) / 2 + 1) * count, 256, s, v, out, n, count, trl, trr);
 }
 template <class T>
 void launch_fiber_thomas(const T* v, T* out, int64_t n, int64_t count, const T* mult,
@@ -444,8 +469,10 @@ void launch_fiber_thomas(const T* v, T* out, int64_t n, int64_t count, const T* 
                                      bool, cudaStream_t);                                    \
   template void check_finite<T>(const T*, int64_t, int*, cudaStream_t);                     \
   template void launch_fiber_mass<T>(const T*, T*, int64_t, int64_t, const T*, cudaStream_t); \
-  template void launch_fiber_masstrans<T>(const T*, T*, int64_t, int64_t, const T*,          \
+  template void launch_fiber_masstrans<T>(const T*, T*, int64_t, int64_t, const T*, bool,    \
                                           cudaStream_t);                                     \
+  template void launch_fiber_transfer<T>(const T*, T*, int64_t, int64_t, const T*, const T*, \
+                                         cudaStream_t);                                      \
   template void launch_fiber_thomas<T>(const T*, T*, int64_t, int64_t, const T*, const T*,   \
                                        const T*, cudaStream_t);
 

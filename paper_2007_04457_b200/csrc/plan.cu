@@ -12,6 +12,7 @@
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
 #include "plan.hpp"
+#include "tables.hpp"
 
 namespace hgrb {
 
@@ -73,7 +74,31 @@ int Plan::sync_status(cudaStream_t s) {
   return *h_flag_ ? HGR_ERR_NONFINITE : HGR_OK;
 }
 
+void Plan::begin_use(cudaStream_t s) {
+  if (!use_ev_) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HGR_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+  if (cs == cudaStreamCaptureStatusNone) HGR_CUDA_CHECK(cudaStreamWaitEvent(s, use_ev_, 0));
+}
+
+void Plan::end_use(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  if (!use_ev_ && cudaEventCreateWithFlags(&use_ev_, cudaEventDisableTiming) != cudaSuccess) {
+    use_ev_ = nullptr;
+    return;
+  }
+  cudaEventRecord(use_ev_, s);
+}
+
 Plan::~Plan() {
+  if (use_ev_) cudaEventDestroy(use_ev_);
+  for (void* p : host_dev_) cudaFree(p);
+  for (void* p : host_pin_) cudaFreeHost(p);
+  for (cudaStream_t st : host_streams_)
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t e : host_ev_)
+    if (e) cudaEventDestroy(e);
   for (auto& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (gstream_) cudaStreamDestroy(gstream_);
@@ -194,73 +219,6 @@ void Plan::run_graphed(int dir, const void* in, const void* out, int m, cudaStre
 
 namespace {
 
-// MassTransOperator<T> taps (correction.hpp:96-133), computed in T exactly as
-// the reference does (spacings cast to T, refined_node_weights in T).
-template <class T>
-std::vector<T> masstrans_taps(const std::vector<T>& h) {
-  const std::size_t nf = h.size() + 1, nc = (nf - 1) / 2 + 1;
-  auto main_ = [&](std::size_t i) {
-    const T left = i > 0 ? h[i - 1] : T(0);
-    const T right = i + 1 < nf ? h[i] : T(0);
-    return T(2) * (left + right);
-  };
-  auto mass_entry = [&](std::size_t t, std::size_t j) -> T {
-    if (j == t) return main_(t);
-    if (j + 1 == t) return h[t - 1];
-    if (j == t + 1) return h[t];
-    return T(0);
-  };
-  std::vector<T> taps(nc * 5, T(0));
-  for (std::size_t i = 0; i < nc; ++i) {
-    std::size_t rj[3];
-    T rw[3];
-    std::size_t rn = 0;
-    if (i > 0) {
-      const T span = h[2 * i - 2] + h[2 * i - 1];
-      rj[rn] = 2 * i - 1;
-      rw[rn++] = h[2 * i - 2] / span;  // to_right
-    }
-    rj[rn] = 2 * i;
-    rw[rn++] = T(1);
-    if (i + 1 < nc) {
-      const T span = h[2 * i] + h[2 * i + 1];
-      rj[rn] = 2 * i + 1;
-      rw[rn++] = h[2 * i + 1] / span;  // to_left
-    }
-    for (std::size_t k = 0; k < 5; ++k) {
-      const long j = long(2 * i) - 2 + long(k);
-      if (j < 0 || j >= long(nf)) continue;
-      T sum = T(0);
-      for (std::size_t r = 0; r < rn; ++r) sum += rw[r] * mass_entry(rj[r], std::size_t(j));
-      taps[i * 5 + k] = sum;
-    }
-  }
-  return taps;
-}
-
-// ThomasSolver<T> factors (correction.hpp:188-198)
-template <class T>
-void thomas_factors(const std::vector<T>& h, std::vector<T>& mult, std::vector<T>& pivot,
-                    std::vector<T>& upper, std::vector<T>& rpiv) {
-  const std::size_t n = h.size() + 1;
-  auto main_ = [&](std::size_t i) {
-    const T left = i > 0 ? h[i - 1] : T(0);
-    const T right = i + 1 < n ? h[i] : T(0);
-    return T(2) * (left + right);
-  };
-  pivot.assign(n, T(0));
-  mult.assign(n > 1 ? n - 1 : 1, T(0));
-  upper.assign(n > 1 ? n - 1 : 1, T(0));
-  rpiv.assign(n, T(0));
-  for (std::size_t i = 0; i < n; ++i) pivot[i] = main_(i);
-  for (std::size_t i = 0; i + 1 < n; ++i) upper[i] = h[i];
-  for (std::size_t i = 1; i < n; ++i) {
-    mult[i - 1] = h[i - 1] / pivot[i - 1];
-    pivot[i] = main_(i) - mult[i - 1] * upper[i - 1];
-  }
-  for (std::size_t i = 0; i < n; ++i) rpiv[i] = T(1) / pivot[i];
-}
-
 template <class T>
 class PlanT final : public Plan {
  public:
@@ -276,6 +234,8 @@ class PlanT final : public Plan {
   void interpolate_to_fine(int level, const void* coarse, void* fine, cudaStream_t s) override;
   void compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) override;
   void compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) override;
+  void apply_coefficients(int level, const void* coarse, const void* coeffs, void* fine,
+                          cudaStream_t s) override;
   void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) override;
 
   void decompose_to(const void* d_in, void* d_out, cudaStream_t s) override;
@@ -329,6 +289,11 @@ class PlanT final : public Plan {
   std::vector<T*> D_;                  // compact coefficient arrays 1..L-1 (decompose)
   std::vector<T*> Z_;                  // corrections 1..L
   T* stage_[2] = {nullptr, nullptr};
+  // LPK stage buffers of a fused-size level that had to take the reference
+  // path (an operand the TMA kernels reject, e.g. a user pointer that is not
+  // 16-byte aligned): allocated on first use, sized for that level
+  T* stage_fb_[2] = {nullptr, nullptr};
+  T* const* stages_for(int l);
   T* W_ = nullptr;                     // scratch of the windowed (out-of-place) Thomas passes
   // coarse tail: levels 1..tail_lt_ (all below the fused threshold, under the
   // top) run as one single-CTA launch per direction (kernels_tail.cu)
@@ -390,13 +355,8 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
       o.taps = push(masstrans_taps<T>(hT));
       o.h = push(hT);
       {
-        // transfer weights in T (refined_node_weights<T>, correction.hpp:76-84)
-        const std::size_t nc = hT.size() / 2 + 1;
-        std::vector<T> trl(nc, T(0)), trr(nc, T(0));
-        for (std::size_t q = 0; q < nc; ++q) {
-          if (q > 0) trl[q] = hT[2 * q - 2] / (hT[2 * q - 2] + hT[2 * q - 1]);
-          if (q + 1 < nc) trr[q] = hT[2 * q + 1] / (hT[2 * q] + hT[2 * q + 1]);
-        }
+        std::vector<T> trl, trr;
+        transfer_weights<T>(hT, trl, trr);
         o.trl = push(trl);
         o.trr = push(trr);
       }
@@ -520,11 +480,35 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
 
 template <class T>
 PlanT<T>::~PlanT() {
+  cudaFree(stage_fb_[0]);
+  cudaFree(stage_fb_[1]);
   cudaFree(tables_);
   cudaFree(ws_);
   cudaFree(tail_dev_);
   cudaFree(d_flag_);
   cudaFreeHost(h_flag_);
+}
+
+// LPK stage buffers for the reference path of level l: the shared ones for
+// small levels, lazily grown fallback buffers for fused-size levels
+template <class T>
+T* const* PlanT<T>::stages_for(int l) {
+  if (!big(l)) return stage_;
+  if (!stage_fb_[0]) {  // sized once for every fused-size level (the top one dominates)
+    std::size_t need[2] = {1, 1};
+    for (int lv = 1; lv <= L(); ++lv) {
+      if (!big(lv)) continue;
+      std::array<int64_t, 3> e = ext_[std::size_t(lv)];
+      int pass = 0;
+      for (int k = 3 - h.rank; k < 2; ++k, ++pass) {
+        e[std::size_t(k)] = ext_[std::size_t(lv) - 1][std::size_t(k)];
+        need[pass & 1] = std::max(need[pass & 1], std::size_t(e[0] * e[1] * e[2]));
+      }
+    }
+    HGR_CUDA_CHECK(cudaMalloc(&stage_fb_[0], need[0] * sizeof(T)));
+    HGR_CUDA_CHECK(cudaMalloc(&stage_fb_[1], need[1] * sizeof(T)));
+  }
+  return stage_fb_;
 }
 
 // correction_level (correction.hpp:295-340): LPK passes over the real dims in
@@ -536,9 +520,10 @@ void PlanT<T>::correction(int l, const T* in, T* z, T* apply, int sign, cudaStre
   const int rank = h.rank;
   int64_t e[3] = {a.e[0], a.e[1], a.e[2]};
   const T* cur = in;
+  T* const* stage = stages_for(l);
   int pass = 0;
   for (int k = 3 - rank; k < 3; ++k, ++pass) {
-    T* dst = (k == 2) ? z : stage_[pass & 1];
+    T* dst = (k == 2) ? z : stage[pass & 1];
     const double n_in = double(e[0] * e[1] * e[2]);
     prof_begin(kKindSmall, sz() * (n_in + n_in / double(e[k]) * double(a.c[k])), s);
     launch_lpk<T>(cur, e, dst, k, a.c[k], a.taps[k], pass == 0, s);
@@ -699,7 +684,15 @@ void PlanT<T>::decompose_to(const void* d_in, void* d_out, cudaStream_t s) {
   // about to be overwritten anyway), for callers that never call autotune()
   if (auto_tune_pending_) {
     auto_tune_pending_ = false;
-    if (!profiling_) autotune(d_in, d_out, s);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    HGR_CUDA_CHECK(cudaStreamIsCapturing(s, &cs));
+    if (!profiling_ && cs == cudaStreamCaptureStatusNone) {
+      try {
+        autotune(d_in, d_out, s);
+      } catch (const Error&) {
+        reset_tuning();  // tuning is an optimisation: keep the heuristics
+      }
+    }
   }
   run_graphed(0, d_in, d_out, 0, s, [&](cudaStream_t st) { decompose_to_direct(d_in, d_out, st); });
 }
@@ -843,6 +836,16 @@ void PlanT<T>::interpolate_to_fine(int level, const void* coarse, void* fine, cu
 }
 
 template <class T>
+void PlanT<T>::apply_coefficients(int level, const void* coarse, const void* coeffs, void* fine,
+                                  cudaStream_t s) {
+  require(level >= 1 && level <= L(), "level out of range");
+  launch_interpolate<T>(static_cast<const T*>(coarse), static_cast<T*>(fine),
+                        args_[std::size_t(level)], s);
+  launch_axpy<T>(static_cast<T*>(fine), static_cast<const T*>(coeffs),
+                 int64_t(h.node_count(level)), +1, s);
+}
+
+template <class T>
 void PlanT<T>::compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) {
   require(level >= 1 && level <= L(), "level out of range");
   launch_coefficients<T>(static_cast<const T*>(fine), static_cast<T*>(coeffs),
@@ -873,6 +876,7 @@ void PlanT<T>::reset_tuning() {
 template <class T>
 std::string PlanT<T>::autotune(const void* d_in, void* d_out, cudaStream_t s) {
   require(!profiling_, "autotune: disable profiling first");
+  auto_tune_pending_ = false;  // an explicit tuning is not redone implicitly
   const int Lv = L();
   const T* in = static_cast<const T*>(d_in);
   T* out = static_cast<T*>(d_out);

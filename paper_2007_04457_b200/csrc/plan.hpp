@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -86,6 +87,9 @@ class Plan {
   virtual void interpolate_to_fine(int level, const void* coarse, void* fine, cudaStream_t s) = 0;
   virtual void compute_coefficients(int level, const void* fine, void* coeffs, cudaStream_t s) = 0;
   virtual void compute_correction(int level, const void* coeffs, void* z, cudaStream_t s) = 0;
+  // apply_coefficients (transforms.hpp:115-124): fine = interp(coarse) + coeffs
+  virtual void apply_coefficients(int level, const void* coarse, const void* coeffs, void* fine,
+                                  cudaStream_t s) = 0;
   virtual void class_copy(void* data, int cls, void* values, bool extract, cudaStream_t s) = 0;
 
   // Tile-segment autotuning (perf_model.hpp:71-137): for every
@@ -98,7 +102,24 @@ class Plan {
   // drop the tuning (back to the built-in heuristics)
   virtual void reset_tuning() = 0;
 
+  // Exclusive use of the plan (workspace, flag, graphs) for one call, the
+  // reference's "distinct arrays may be processed concurrently" contract
+  // (SPEC.md:287): host threads are serialised by `use_mu`, and a call's work
+  // on its stream is ordered after the previous call's by an event recorded
+  // at the end of every call, so two streams never share the workspace at the
+  // same time. Skipped while the caller's stream is being captured.
+  std::recursive_mutex use_mu;
+  void begin_use(cudaStream_t s);
+  void end_use(cudaStream_t s);
+  // device staging of the host-pointer entry points (allocated on first use)
+  void* host_dev_[2] = {nullptr, nullptr};
+  void* host_pin_[2] = {nullptr, nullptr};
+  std::size_t host_pin_bytes_ = 0;
+  cudaStream_t host_streams_[2] = {nullptr, nullptr};
+  cudaEvent_t host_ev_[4] = {nullptr, nullptr, nullptr, nullptr};
+
  protected:
+  cudaEvent_t use_ev_ = nullptr;
   int* d_flag_ = nullptr;   // non-finite flag set by the level-L decompose kernel
   int* h_flag_ = nullptr;   // pinned mirror
 
@@ -142,6 +163,10 @@ class Plan {
 };
 
 std::unique_ptr<Plan> make_plan(const hgr_grid_desc* g, int dtype);
+
+// report.cu: error_report (refactor.hpp:100-120) of b against a; synchronizes s
+template <class T>
+void error_report(const T* a, const T* b, int64_t n, double out[4], cudaStream_t s);
 
 // synth.cu
 template <class T>

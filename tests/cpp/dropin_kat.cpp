@@ -10,6 +10,7 @@
 #include <functional>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 using hgr::GridHierarchy;
@@ -190,6 +191,93 @@ int main() {
     ndarray<double> a({2}, {1, 1}), b({2}, {1, 0});
     auto rep = hgr::error_report(a, b);
     return rep.linf_abs == 1.0 && rep.l2_abs == 1.0 && std::abs(rep.l2_rel - 1 / std::sqrt(2.0)) < 1e-15;
+  });
+  // test_correction.cpp:35-107: the operator classes of the drop-in
+  check("TridiagonalOperator::mass_matrix apply [1,1,1,1,1] -> [3,6,6,6,3]", [] {
+    std::vector<double> h{1, 1, 1, 1};
+    auto m = hgr::TridiagonalOperator<double>::mass_matrix(h);
+    return m.size() == 5 && m.apply(std::vector<double>{1, 1, 1, 1, 1}) == std::vector<double>{3, 6, 6, 6, 3} &&
+           m.apply(std::vector<double>{0, -1, 0, -1, 0}) == std::vector<double>{-1, -4, -2, -4, -1};
+  });
+  check("mass_apply float [0,-1,0,-1,0] -> [-1,-4,-2,-4,-1]", [] {
+    std::vector<float> h{1, 1, 1, 1}, c{0, -1, 0, -1, 0};
+    return hgr::mass_apply<float>(c, h) == std::vector<float>{-1, -4, -2, -4, -1};
+  });
+  check("transfer_apply -> [-0.5,-1,-0.5]; h=[1,2] [0,3,0] -> [2,1]", [] {
+    std::vector<double> h{1, 1, 1, 1}, c{0, -1, 0, -1, 0};
+    if (hgr::transfer_apply<double>(c, h) != std::vector<double>{-0.5, -1, -0.5}) return false;
+    std::vector<double> h2{1, 2}, v{0, 3, 0};
+    auto t = hgr::transfer_apply<double>(v, h2);
+    return std::abs(t[0] - 2) < 1e-15 && std::abs(t[1] - 1) < 1e-15 &&
+           hgr::transfer_apply<float>(std::vector<float>{0, -1, 0, -1, 0}, std::vector<float>{1, 1, 1, 1}) ==
+               std::vector<float>{-0.5f, -1, -0.5f};
+  });
+  check("transfer_apply rejects even fibers", [] {
+    std::vector<double> h{1, 1, 1}, v{1, 2, 3, 4};
+    return throws_with([&] { hgr::transfer_apply<double>(v, h); }, "odd");
+  });
+  check("MassTransOperator row 0 = [2.5,3,0.5,0,0]; apply_fiber masked/strided", [] {
+    std::vector<double> h{1, 1, 1, 1};
+    hgr::MassTransOperator<double> op{std::span<const double>(h)};
+    if (op.fine_size() != 5 || op.coarse_size() != 3) return false;
+    if (op.row(0) != std::vector<double>{2.5, 3, 0.5, 0, 0}) return false;
+    // strided fiber (stride 2) with the even entries masked == the coefficient-only product
+    std::vector<double> in{7, 0, -1, 0, 9, 0, -1, 0, 5, 0}, out(6, 0.0);
+    op.apply_fiber(in.data(), 2, true, out.data(), 2);
+    return out[0] == -3 && out[2] == -6 && out[4] == -3 && out[1] == 0;
+  });
+  check("ThomasSolver solve_fiber h=[2,2] [-3,-6,-3] -> -0.5 (strided)", [] {
+    std::vector<double> h{2, 2};
+    hgr::ThomasSolver<double> t{std::span<const double>(h)};
+    std::vector<double> x{-3, 1, -6, 1, -3, 1};
+    t.solve_fiber(x.data(), 2);
+    return t.size() == 3 && std::abs(x[0] + 0.5) < 1e-15 && std::abs(x[2] + 0.5) < 1e-15 &&
+           std::abs(x[4] + 0.5) < 1e-15 && x[1] == 1;
+  });
+  check("correction_workspace_elements (test_correction.cpp:297)", [] {
+    using hgr::detail::correction_workspace_elements;
+    auto g3 = GridHierarchy::uniform({9, 17, 33});
+    auto g1 = GridHierarchy::uniform({33});
+    return correction_workspace_elements(g3, 3) == 5u * 17 * 33 + 5u * 9 * 33 &&
+           correction_workspace_elements(g1, 2) == 0;
+  });
+  check("detail::correction_level (batched fiber passes) == compute_correction", [] {
+    std::vector<double> a(17), b(9), c(17);
+    for (std::size_t i = 0; i < 17; ++i) a[i] = i + 0.01 * i * i, c[i] = 2.0 * i + std::sin(double(i));
+    for (std::size_t i = 0; i < 9; ++i) b[i] = i * i + i;
+    GridHierarchy g({a, b, c});
+    const int l = g.levels();
+    auto d = ndarray<double>(g.finest_extents(), values<double>(17 * 9 * 17, 5));
+    auto coef = hgr::compute_coefficients(d, g, l);
+    auto z1 = hgr::compute_correction(coef, g, l);
+    ndarray<double> z2(g.level_extents(l - 1));
+    std::vector<double> ws;
+    hgr::detail::correction_level(hgr::as_const(hgr::full_view(coef)), true, g, l, z2, ws);
+    double diff = 0, sc = 0;
+    for (std::size_t i = 0; i < z1.size(); ++i)
+      diff = std::max(diff, std::abs(z1[i] - z2[i])), sc = std::max(sc, std::abs(z1[i]));
+    return ws.size() >= hgr::detail::correction_workspace_elements(g, l) && diff <= 1e-13 * sc;
+  });
+  check("concurrent decompose of distinct arrays on one grid == serial (bitwise)", [] {
+    auto g = GridHierarchy::uniform({33, 33, 65});
+    std::vector<ndarray<double>> in;
+    for (int t = 0; t < 4; ++t) in.emplace_back(g.finest_extents(), values<double>(33 * 33 * 65, 10 + t));
+    std::vector<ndarray<double>> serial, par(4);
+    for (int t = 0; t < 4; ++t) serial.push_back(hgr::decompose(in[std::size_t(t)], g).data);
+    for (int rep = 0; rep < 3; ++rep) {
+      std::vector<std::thread> th;
+      for (int t = 0; t < 4; ++t)
+        th.emplace_back([&, t] { par[std::size_t(t)] = hgr::decompose(in[std::size_t(t)], g).data; });
+      for (auto& x : th) x.join();
+      for (int t = 0; t < 4; ++t)
+        if (!(par[std::size_t(t)] == serial[std::size_t(t)])) return false;
+    }
+    return true;
+  });
+  check("device error_report (float) matches the definition", [] {
+    ndarray<float> a({4}, {1, -2, 3, 4}), b({4}, {1, -2, 2.5f, 4});
+    auto rep = hgr::error_report(a, b);
+    return rep.linf_abs == 0.5 && rep.linf_rel == 0.125 && std::abs(rep.l2_abs - 0.5) < 1e-15;
   });
   std::printf("%d failure(s)\n", failures);
   return failures == 0 ? 0 : 1;
