@@ -26,6 +26,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 PORT_SO = HERE / "lib" / "libhgr_oracle.so"
 REF_SO = HERE / "_ref" / "libhgr_ref.so"
+REF_NATIVE_SO = HERE / "_ref" / "libhgr_ref_native.so"
 REF_INCLUDE = Path("/root/reference/proj/include")
 
 
@@ -59,6 +60,13 @@ class Oracle:
                 build()
             self.lib = C.CDLL(str(PORT_SO))
             self.pfx = "hgro_"
+        elif kind == "reference-native":
+            # the timing build (-O3 -march=native); only where this CPU has every
+            # flag of the build machine
+            if not native_usable():
+                raise OracleError("reference-native build missing or not runnable on this CPU")
+            self.lib = C.CDLL(str(REF_NATIVE_SO))
+            self.pfx = "hgrref_"
         elif kind == "reference":
             if not REF_SO.exists():
                 if REF_INCLUDE.exists():
@@ -199,7 +207,7 @@ class Oracle:
     # storage.hpp (reference only): the .hg container
     def write_file(self, pyramid, path, coords=None):
         """hgr::write_file of a decomposed pyramid; returns the byte count."""
-        assert self.kind == "reference", "the .hg container exists in the reference only"
+        assert self.kind.startswith("reference"), "the .hg container exists in the reference only"
         src = np.ascontiguousarray(pyramid)
         g, _k = self._grid(src.shape, coords)
         n = C.c_ulonglong(0)
@@ -209,7 +217,7 @@ class Oracle:
 
     def read_prefix(self, path, upto_class, shape, dtype):
         """hgr::read_prefix: (zero-filled pyramid, bytes_read)."""
-        assert self.kind == "reference", "the .hg container exists in the reference only"
+        assert self.kind.startswith("reference"), "the .hg container exists in the reference only"
         out = np.zeros(shape, dtype=dtype)
         n = C.c_ulonglong(0)
         self._check(self._fn("read_prefix_" + _dt(out))(str(path).encode(), int(upto_class),
@@ -217,18 +225,33 @@ class Oracle:
         return out, int(n.value)
 
     def set_worker_count(self, n: int) -> None:
-        if self.kind != "reference":
+        if not self.kind.startswith("reference"):
             return
         self.lib.hgrref_set_worker_count(C.c_size_t(n))
 
     def worker_count(self) -> int:
-        if self.kind != "reference":
+        if not self.kind.startswith("reference"):
             return 1
         self.lib.hgrref_worker_count.restype = C.c_size_t
         return int(self.lib.hgrref_worker_count())
 
 
+def native_usable() -> bool:
+    """True if oracle/_ref/libhgr_ref_native.so exists and this CPU has every
+    feature flag of the machine it was compiled on (-march=native)."""
+    flags_file = HERE / "_ref" / "native_flags.txt"
+    if not (REF_NATIVE_SO.exists() and flags_file.exists()):
+        return False
+    try:
+        here = next(l for l in open("/proc/cpuinfo") if l.startswith("flags")).split(":", 1)[1].split()
+    except (OSError, StopIteration):
+        return False
+    return set(flags_file.read_text().split()) <= set(here)
+
+
 def available(kind: str) -> bool:
+    if kind == "reference-native":
+        return native_usable()
     return PORT_SO.exists() if kind == "port" else REF_SO.exists()
 
 

@@ -363,7 +363,7 @@ def error_report(original, reconstruction) -> ErrorReport:
     current CUDA device."""
     if tuple(original.shape) != tuple(reconstruction.shape):
         raise HgrError("error_report: shape mismatch")
-    if original.numel() if _is_torch(original) else np.size(original) == 0:
+    if (original.numel() if _is_torch(original) else np.size(original)) == 0:
         return ErrorReport()
     a, _ = _to_device(original)
     b, _ = _to_device(reconstruction)

@@ -3,6 +3,8 @@
 // and serve the coarse levels and the single-level API; the fine levels use
 // the fused kernels in kernels_fused.cu / kernels_thomas.cu.
 #include <cstdio>
+#include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "launch.cuh"
@@ -12,9 +14,43 @@
 namespace hgrb {
 
 [[noreturn]] void throw_cuda(cudaError_t e, const char* expr, const char* file, int line) {
+  cudaGetLastError();  // reported here; a non-sticky error must not resurface in a later check
   char buf[512];
   std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
                 cudaGetErrorString(e), file, line, expr);
+  throw Error(HGR_ERR_CUDA, buf);
+}
+
+void set_smem_attr(const void* fn, size_t bytes) {
+  struct Set {
+    int dev;
+    const void* fn;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Set> done;
+  int dev = 0;
+  HGR_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& d : done)
+    if (d.dev == dev && d.fn == fn) {
+      if (d.bytes >= bytes) return;
+      HGR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+      d.bytes = bytes;
+      return;
+    }
+  HGR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  done.push_back(Set{dev, fn, bytes});
+}
+
+[[noreturn]] void launch_failed(cudaError_t e, const void* kern, dim3 grid, dim3 block, size_t smem) {
+  cudaGetLastError();  // a failed launch is not sticky: do not let it leak into later checks
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, kern) != cudaSuccess || !name) name = "?";
+  char buf[768];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) launching %s grid (%u,%u,%u) block (%u,%u,%u) smem %zu",
+                cudaGetErrorName(e), cudaGetErrorString(e), name, grid.x, grid.y, grid.z, block.x,
+                block.y, block.z, smem);
   throw Error(HGR_ERR_CUDA, buf);
 }
 

@@ -436,14 +436,7 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
                 cudaStream_t s, int s0) {
   using Cf = ICfg<T>;
   auto kern = k_interp_march<T, WITH, HASZ>;
-  static int attr_dev = -1;
-  int dev = 0;
-  HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    HGR_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(Cf::total)));
-    attr_dev = dev;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(kern), Cf::total);
   const int nt1 = int((a.c[1] - 1 + Cf::TW1 - 1) / Cf::TW1);
   const int nt2 = int((a.c[2] - 1 + Cf::TW2 - 1) / Cf::TW2);
   const int64_t tiles = int64_t(nt1) * nt2;

@@ -724,16 +724,7 @@ __global__ void __launch_bounds__(256)
 
 template <class T, int MODE>
 void set_level_face_smem(size_t bytes) {
-  static size_t set_bytes = 48 * 1024;
-  static int set_dev = -1;
-  int dev = 0;
-  HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  if (bytes > 48 * 1024 && (bytes > set_bytes || dev != set_dev)) {
-    HGR_CUDA_CHECK(cudaFuncSetAttribute(k_level_face<T, MODE>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-    set_bytes = bytes;
-    set_dev = dev;
-  }
+  if (bytes > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(k_level_face<T, MODE>), bytes);
 }
 
 template <class T>
@@ -757,14 +748,7 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
                cudaStream_t s, int s0) {
   using C = LCfg<T>;
   auto kern = k_level_fused<T, MODE>;
-  static int attr_dev = -1;
-  int dev = 0;
-  HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    HGR_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        int(C::total)));
-    attr_dev = dev;
-  }
+  set_smem_attr(reinterpret_cast<const void*>(kern), C::total);
   const int nt1 = int((a.c[1] - 1 + C::TW1 - 1) / C::TW1);
   const int nt2 = int((a.c[2] - 1 + C::TW2 - 1) / C::TW2);
   const int64_t tiles = int64_t(nt1) * nt2;

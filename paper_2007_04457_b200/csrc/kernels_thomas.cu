@@ -747,19 +747,6 @@ int sm_count() {
   return sms;
 }
 
-// raise a kernel's dynamic shared-memory limit once per (device, kernel, size)
-void set_smem_attr(const void* fn, size_t bytes) {
-  struct Seen { int dev; const void* fn; size_t bytes; };
-  static thread_local Seen seen[64];
-  static thread_local int nseen = 0;
-  int dev = 0;
-  HGR_CUDA_CHECK(cudaGetDevice(&dev));
-  for (int i = 0; i < nseen; ++i)
-    if (seen[i].dev == dev && seen[i].fn == fn && seen[i].bytes >= bytes) return;
-  HGR_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-  if (nseen < 64) seen[nseen++] = Seen{dev, fn, bytes};
-}
-
 template <class T, int CH, int R>
 void run_rows(const T* in, T* out, int64_t rows, int64_t n, const T* mult, const T* rpiv,
               const T* upper, cudaStream_t s) {

@@ -28,6 +28,15 @@ inline bool pdl_for(int64_t level_nodes) {
   return level_nodes < lim;
 }
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+// current device. Process-wide and only ever raised (under a mutex): a
+// per-thread record could let one thread lower the limit below what another
+// thread's later launch needs. (kernels_basic.cu)
+void set_smem_attr(const void* fn, size_t bytes);
+
+// throws with the kernel name and launch geometry in the message (kernels_basic.cu)
+[[noreturn]] void launch_failed(cudaError_t e, const void* kern, dim3 grid, dim3 block, size_t smem);
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                 int64_t level_nodes, Args&&... args) {
@@ -41,7 +50,8 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  HGR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) launch_failed(e, reinterpret_cast<const void*>(kern), grid, block, smem);
 }
 
 }  // namespace hgrb

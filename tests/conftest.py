@@ -32,3 +32,24 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    """Record a parity measurement: printed (pytest -s / -rA) and appended as a
+    JSON line to $HGR_PARITY_LOG (default gpurun_out/parity_errors.jsonl when
+    that directory exists), so the measured error headroom can be tracked
+    between rounds."""
+    import json
+    import os
+    path = os.environ.get("HGR_PARITY_LOG")
+    if not path and (ROOT / "gpurun_out").is_dir():
+        path = str(ROOT / "gpurun_out" / "parity_errors.jsonl")
+
+    def log(test: str, **values):
+        rec = {"test": test, **values}
+        print("PARITY " + json.dumps(rec))
+        if path:
+            with open(path, "a") as f:
+                f.write(json.dumps(rec) + "\n")
+    return log

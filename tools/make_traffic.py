@@ -46,6 +46,12 @@ for arg in sys.argv[1:]:
         tot = sum(l.get('dram__bytes_read.sum', 0) + l.get('dram__bytes_write.sum', 0) for l in sel)
         # one bench bracket per main-kernel launch (faces share their level's bracket)
         cls[kind] = round(tot / len(main))
+    # the whole round trip: every launch's DRAM bytes and time (bench dram_frac)
+    cls["_step"] = {
+        "dram_bytes": round(sum(l.get('dram__bytes_read.sum', 0) + l.get('dram__bytes_write.sum', 0)
+                                for l in launches)),
+        "kernel_ms": round(sum(l.get('gpu__time_duration.sum', 0) for l in launches) / 1e6, 4),
+        "launches": len(launches), "source": Path(path).name}
     res[cfg] = cls
     print(cfg, cls)
 out_path.write_text(json.dumps(res, indent=1) + "\n")
