@@ -23,6 +23,18 @@ bool launch_thomas_fast(const T* in, T* out, const int64_t ext[3], int dim, cons
 template <class T>
 bool thomas_needs_out_of_place(const int64_t ext[3], int dim);
 
+// IPK of a 3D level in two passes (kernels_band.cu): dim 0 in place on src (the
+// strided-line kernel, or a cluster band pass when band_dim0), then dims 1 + 2
+// fused per dim-0 plane by thread-block clusters from src into dst (src is
+// clobbered; dst may equal src). Returns false (nothing launched) when the
+// coarse extents or operands do not fit.
+template <class T>
+bool thomas_band_supported(const int64_t c[3]);
+template <class T>
+bool launch_thomas_planes(T* src, T* dst, const int64_t c[3], const T* const mult[3],
+                          const T* const rpiv[3], const T* const upper[3], int64_t level_nodes,
+                          bool band_dim0, cudaStream_t s);
+
 // The coarse tail (kernels_tail.cu): levels 1..lt of a plan in one CTA per
 // direction. Per level: its arguments and compact buffers.
 template <class T>

@@ -299,6 +299,11 @@ class PlanT final : public Plan {
   // top) run as one single-CTA launch per direction (kernels_tail.cu)
   int tail_lt_ = 0;
   bool auto_tune_pending_ = false;  // HGR_AUTOTUNE=1
+  // 3D IPK as dim 0 + fused dims 1+2 (kernels_band.cu); knob HGR_THOMAS_BAND:
+  // 0 three passes, 1 strided-line dim 0 + cluster planes, 2 cluster passes for
+  // both. Default: 1 for fp32, 0 for fp64 (its 135 KB plane tiles leave one
+  // single-buffered CTA per SM; measured slower than three passes)
+  int band_thomas_ = sizeof(T) == 4 ? 1 : 0;
   TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
   std::vector<int> s0_dec_, s0_rec_, s0_int_;
@@ -317,6 +322,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   big_nodes_ = h.rank == 3 ? std::size_t(1) << 15 : std::size_t(4096);
   if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
   if (const char* v = std::getenv("HGR_AUTOTUNE")) auto_tune_pending_ = v[0] == '1';
+  if (const char* v = std::getenv("HGR_THOMAS_BAND")) band_thomas_ = std::atoi(v);
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   s0_dec_.assign(std::size_t(h.L) + 1, 0);
   s0_rec_.assign(std::size_t(h.L) + 1, 0);
@@ -585,6 +591,17 @@ template <class T>
 void PlanT<T>::thomas_all(int l, T* src, T* last_out, cudaStream_t s) {
   const LevelArgs<T>& a = args_[std::size_t(l)];
   const int64_t c[3] = {a.c[0], a.c[1], a.c[2]};
+  if (h.rank == 3 && band_thomas_) {
+    // two cluster passes: dim 0 in place, dims 1 + 2 fused into last_out
+    prof_begin(kKindThomas, sz() * 4.0 * double(c[0] * c[1] * c[2]), s);
+    const bool ok = launch_thomas_planes<T>(src, last_out, c, a.mult, a.rpiv, a.upper,
+                                            int64_t(h.node_count(l)), band_thomas_ == 2, s);
+    prof_end(s);
+    if (ok) {
+      launch_count_ += 2;
+      return;
+    }
+  }
   T* cur = src;
   for (int k = 3 - h.rank; k < 3; ++k) {
     T* dst = cur;
