@@ -2,7 +2,9 @@
 // output / line. They define the GPU semantics of every step of the hot path
 // and serve the coarse levels and the single-level API; the fine levels use
 // the fused kernels in kernels_fused.cu / kernels_thomas.cu.
+#include <algorithm>
 #include <cstdio>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -282,6 +284,117 @@ __global__ void __launch_bounds__(256) k_scatter_even(const T* __restrict__ src,
   }
 }
 
+// Even rows of even planes of a level decomposed with side rows, written whole:
+// even columns from the compact coarser pyramid, odd columns from the side rows.
+// Persistent CTAs stream rows through an NST-stage ring: the coarse row and the
+// side row arrive as bulk copies (their 16-byte aligned supersets), every thread
+// assembles one aligned 16-byte output vector from shared memory and stores it
+// -- full-sector writes instead of the strided scatter's read-modify-writes.
+constexpr int kMergeStages = 3, kMergeRows = 4;  // ring stages x rows per stage
+template <class T>
+struct MergeCfg {
+  static constexpr int V = 16 / int(sizeof(T));
+  static __host__ __device__ int64_t row_elems(int64_t c2) { return (c2 + 2 * V - 1) / V * V; }  // superset + slack
+  static size_t smem(int64_t c2) {
+    return size_t(kMergeStages) * kMergeRows * 2 * size_t(row_elems(c2)) * sizeof(T) + kMergeStages * 8;
+  }
+};
+
+template <class T>
+__global__ void __launch_bounds__(1024) k_merge_even(const T* __restrict__ coarse,
+                                                     const T* __restrict__ side, T* __restrict__ out,
+                                                     LevelArgs<T> a) {
+  ptx::pdl_trigger();
+  constexpr int V = MergeCfg<T>::V;
+  using VT = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  const int64_t c1 = a.c[1], c2 = a.c[2], e1 = a.e[1], e2 = a.e[2];
+  const int64_t rows = a.c[0] * c1, RE = MergeCfg<T>::row_elems(c2);
+  extern __shared__ __align__(16) unsigned char smem_m[];
+  constexpr int R = kMergeRows;
+  T* ring = reinterpret_cast<T*>(smem_m);  // [stage][row][coarse row | side row]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ring + kMergeStages * R * 2 * RE);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int k = 0; k < kMergeStages; ++k) ptx::mbar_init(&bar[k], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t groups = (rows + R - 1) / R;  // a group = R consecutive rows
+  auto issue = [&](int64_t grp, int st) {     // tid 0
+    uint32_t total = 0;
+    for (int r = 0; r < R; ++r) {
+      const int64_t rr = grp * R + r;
+      if (rr >= rows) break;
+      const int64_t cb = rr * c2, sb = rr * (c2 - 1);
+      const int pc = int(cb & (V - 1)), ps = int(sb & (V - 1));
+      total += uint32_t((pc + c2 + V - 1) / V * V * sizeof(T)) +
+               uint32_t((ps + c2 - 1 + V - 1) / V * V * sizeof(T));
+    }
+    ptx::mbar_arrive_expect_tx(&bar[st], total);
+    for (int r = 0; r < R; ++r) {
+      const int64_t rr = grp * R + r;
+      if (rr >= rows) break;
+      const int64_t cb = rr * c2, sb = rr * (c2 - 1);
+      const int pc = int(cb & (V - 1)), ps = int(sb & (V - 1));
+      T* dst = ring + (int64_t(st) * R + r) * 2 * RE;
+      ptx::bulk_g2s(dst, coarse + (cb - pc), uint32_t((pc + c2 + V - 1) / V * V * sizeof(T)), &bar[st]);
+      ptx::bulk_g2s(dst + RE, side + (sb - ps), uint32_t((ps + c2 - 1 + V - 1) / V * V * sizeof(T)),
+                    &bar[st]);
+    }
+  };
+  const int64_t G = gridDim.x;
+  ptx::pdl_wait();
+  if (tid == 0)
+    for (int k = 0; k < kMergeStages; ++k)
+      if (blockIdx.x + k * G < groups) issue(blockIdx.x + k * G, k);
+  int it = 0;
+  for (int64_t grp = blockIdx.x; grp < groups; grp += G, ++it) {
+    const int st = it % kMergeStages;
+    ptx::mbar_wait(&bar[st], uint32_t((it / kMergeStages) & 1));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t rr = grp * R + r;
+      if (rr >= rows) break;
+      const T* base = ring + (int64_t(st) * R + r) * 2 * RE;
+      const T* cr = base + int((rr * c2) & (V - 1));
+      const T* sr = base + RE + int((rr * (c2 - 1)) & (V - 1));
+      const int64_t q0 = rr / c1, q1 = rr - q0 * c1;
+      const int64_t g = ((2 * q0) * e1 + 2 * q1) * e2;
+      const int ph = int(g & (V - 1));
+      const int nvec = int((ph + e2 + V - 1) / V);
+      T* orow = out + (g - ph);
+      for (int u = tid; u < nvec; u += blockDim.x) {
+        T v[V];
+        bool full = true;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const int p = u * V + k - ph;
+          const bool in = p >= 0 && p < e2;
+          full = full && in;
+          v[k] = !in ? T(0) : (p & 1) ? sr[p >> 1] : cr[p >> 1];
+        }
+        if (full) {
+          VT w;
+          if constexpr (V == 4) {
+            w.x = v[0]; w.y = v[1]; w.z = v[2]; w.w = v[3];
+          } else {
+            w.x = v[0]; w.y = v[1];
+          }
+          reinterpret_cast<VT*>(orow)[u] = w;
+        } else {
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const int p = u * V + k - ph;
+            if (p >= 0 && p < e2) orow[u * V + k] = v[k];
+          }
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with this stage: refill it
+    if (tid == 0 && grp + kMergeStages * G < groups) issue(grp + kMergeStages * G, st);
+  }
+}
+
 // Rank of level-cls node (i0,i1,i2) among the class-cls nodes in row-major
 // order, skipping all-even indices (refactor.hpp:134-145).
 __device__ __forceinline__ int64_t class_rank(int64_t i0, int64_t i1, int64_t i2, int64_t e1,
@@ -438,6 +551,22 @@ void launch_gather(const T* src, const int64_t se[3], int64_t stride, T* dst,
              dst, de[0], de[1], de[2]);
 }
 template <class T>
+void launch_merge_even(const T* coarse, const T* side, T* out, const LevelArgs<T>& a,
+                       cudaStream_t s) {
+  constexpr int64_t V = MergeCfg<T>::V;
+  const int64_t nvec = (a.e[2] + 2 * V - 2) / V;
+  const int threads = int(std::min<int64_t>(1024, (nvec + 31) / 32 * 32));
+  const size_t smem = MergeCfg<T>::smem(a.c[2]);
+  require(smem <= 200 * 1024, "merge_even: rows too long for the shared-memory ring");
+  set_smem_attr(reinterpret_cast<const void*>(k_merge_even<T>), smem);
+  int per_sm = 0;
+  HGR_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_even<T>, threads, smem));
+  const int64_t groups = (a.c[0] * a.c[1] + kMergeRows - 1) / kMergeRows;
+  const int64_t grid = grid_for(groups * threads, threads, std::max(1, per_sm));
+  launch_pdl(k_merge_even<T>, dim3(unsigned(grid)), dim3(threads), smem, s, a.e[0] * a.e[1] * a.e[2],
+             coarse, side, out, a);
+}
+template <class T>
 void launch_scatter_even(const T* src, T* dst, const LevelArgs<T>& a, cudaStream_t s) {
   const int64_t items = a.c[0] * a.c[1] * ((a.c[2] + kRowSeg - 1) / kRowSeg);  // a warp each
   launch_pdl(k_scatter_even<T>, dim3(grid_for(items * 32, 256)), dim3(256), 0, s,
@@ -498,6 +627,7 @@ void launch_fiber_thomas(const T* v, T* out, int64_t n, int64_t count, const T* 
   template void launch_gather<T>(const T*, const int64_t*, int64_t, T*, const int64_t*,      \
                                  cudaStream_t);                                              \
   template void launch_scatter_even<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);     \
+  template void launch_merge_even<T>(const T*, const T*, T*, const LevelArgs<T>&, cudaStream_t); \
   template void launch_coefficients<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);     \
   template void launch_interpolate<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);      \
   template void launch_check_coarse_zero<T>(const T*, const LevelArgs<T>&, int*, cudaStream_t); \

@@ -65,9 +65,21 @@ enum FusedMode : int {
 // Returns false if the level is not supported (caller falls back).
 // flag (decompose mode, may be null): set to 1 if any input value is NaN/Inf.
 // s0: coarse planes per CTA segment along dim 0 (0 = built-in heuristic).
+// side (decompose mode, 2D / 3D, may be null): the coefficients on even rows of
+// even planes (odd columns only) go to the compact side rows
+// side[((j/2)*c1 + r/2)*(c2-1) + (c-1)/2] instead of coef_out, and those output
+// rows are left for launch_merge_even.
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
-                        int mode, int* flag, cudaStream_t s, int s0 = 0);
+                        int mode, int* flag, cudaStream_t s, int s0 = 0, T* side = nullptr);
+
+// Pyramid assembly of a level decomposed with side rows: every even row of an
+// even plane of `out` (level-l extents e) is written whole, its even columns
+// from the finished level-(l-1) pyramid `coarse` (compact c) and its odd
+// columns from the side rows -- full-sector writes instead of a strided scatter.
+template <class T>
+void launch_merge_even(const T* coarse, const T* side, T* out, const LevelArgs<T>& a,
+                       cudaStream_t s);
 
 // Recompose interpolation (GPK^-1, refactor.hpp:77-87): coarse = C - Z (Z may be
 // null), out[coarse] = coarse, out[refined] = (with ? coef : 0) + interp(coarse).

@@ -169,8 +169,8 @@ __device__ __forceinline__ void loadV(const T* row, int ph, int base, T (&v)[NV]
 template <class T, int MODE>
 __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
     k_level_fused(const __grid_constant__ CUtensorMap map, int64_t map_off, T* __restrict__ coef_out,
-                  T* __restrict__ zload, T* __restrict__ gather, LevelArgs<T> a, int S0, int nt1,
-                  int nt2, int nseg, int seg_base, int* flag) {
+                  T* __restrict__ zload, T* __restrict__ gather, T* __restrict__ side, LevelArgs<T> a,
+                  int S0, int nt1, int nt2, int nseg, int seg_base, int* flag) {
   using C = LCfg<T>;
   using T2 = typename Vec2<T>::type;
   ptx::pdl_trigger();
@@ -525,6 +525,23 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
                   cv[k] = v[2 + k] - A1[k];
                   bad = cv[k] * T(0) + bad;
                 }
+                if (!(i & 1) && side != nullptr) {
+                  // even row of an even plane: its odd cells go to the compact side
+                  // rows; the output row is written whole by k_merge_even
+                  T* sr = side + ((j >> 1) * c1 + ((wr0 + r) >> 1)) * (c2 - 1) + q2a + t0;
+                  if constexpr (CPL == 2) {
+                    if (cvalid[0] && cvalid[1]) {
+                      T2 w;
+                      w.x = cv[1];
+                      w.y = cv[3];
+                      *reinterpret_cast<T2*>(sr) = w;
+                    } else if (cvalid[0]) {
+                      sr[0] = cv[1];
+                    }
+                  } else {
+                    if (cvalid[0]) sr[0] = cv[1];
+                  }
+                } else
                 // the cells' global phase equals the input's: window phase + 2
                 if constexpr (PH >= 0) {
                   if (vstore) {
@@ -637,7 +654,7 @@ constexpr int kFaceSeg = 64, kFaceCells = 256;
 template <class T, int MODE>
 __global__ void __launch_bounds__(256)
     k_level_face(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ zload,
-                 T* __restrict__ gather, LevelArgs<T> a, int* flag) {
+                 T* __restrict__ gather, T* __restrict__ side, LevelArgs<T> a, int* flag) {
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
   ptx::pdl_trigger();
   ptx::pdl_wait();
@@ -717,7 +734,13 @@ __global__ void __launch_bounds__(256)
     const int64_t idx = j * plane + int64_t(r) * e2 + c;
     const T u = U[idx];
     bad |= !isfinite(u);
-    if ((j | r | c) & 1) coef_out[idx] = u - interp_node(a, j, r, c, coarse);
+    if ((j | r | c) & 1) {
+      const T cv = u - interp_node(a, j, r, c, coarse);
+      if (side != nullptr && !((j | r) & 1))  // even row of an even plane (c odd)
+        side[((j >> 1) * int64_t(c1) + (r >> 1)) * (c2 - 1) + (c >> 1)] = cv;
+      else
+        coef_out[idx] = cv;
+    }
   }
   if (flag && __syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
 }
@@ -744,7 +767,7 @@ int fused_heuristic_s0(const LevelArgs<T>& a) {
 }
 
 template <class T, int MODE>
-void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int* flag,
+void run_fused(const T* U, T* coef, T* z, T* gather, T* side, const LevelArgs<T>& a, int* flag,
                cudaStream_t s, int s0) {
   using C = LCfg<T>;
   auto kern = k_level_fused<T, MODE>;
@@ -773,7 +796,7 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
     make_tma_1d(&map, U + map_off, uint64_t(N - map_off), int(sizeof(T)), C::BOX);
     const int64_t blocks = tiles * (sb - sa);
     launch_pdl(kern, dim3(unsigned(blocks)), dim3(C::NT), C::total, s, N, map, map_off, coef, z,
-               gather, a, S0, nt1, nt2, nseg, sa, flag);
+               gather, side, a, S0, nt1, nt2, nseg, sa, flag);
     sa = sb;
   }
   const int64_t fseg =
@@ -784,25 +807,29 @@ void run_fused(const T* U, T* coef, T* z, T* gather, const LevelArgs<T>& a, int*
   const size_t fsmem = size_t(5) * size_t(2 * kFaceSeg + 3) * sizeof(T);
   set_level_face_smem<T, MODE>(fsmem);
   launch_pdl(k_level_face<T, MODE>, fgrid, dim3(256), fsmem, s, a.e[0] * a.e[1] * a.e[2], U, coef,
-             z, gather, a, flag);
+             z, gather, side, a, flag);
 }
 
 }  // namespace
 
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
-                        int mode, int* flag, cudaStream_t s, int s0) {
+                        int mode, int* flag, cudaStream_t s, int s0, T* side) {
   // TMA needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
-  if (a.e[0] == 1 && a.e[1] == 1) return launch_line_level<T>(U, coef_out, zload, gather, a, mode, flag, s);
+  if (a.e[0] == 1 && a.e[1] == 1) {
+    require(side == nullptr, "side rows are a 2D / 3D decompose option");
+    return launch_line_level<T>(U, coef_out, zload, gather, a, mode, flag, s);
+  }
   if ((reinterpret_cast<uintptr_t>(U) & 15) != 0) return false;
   if (a.e[1] < 3 || a.e[2] < 3 || a.h[2] == nullptr) return false;
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
+  require(side == nullptr || mode == kFusedDecompose, "side rows are a decompose option");
   if (mode == kFusedDecompose)
-    run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, a, flag, s, s0);
+    run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, side, a, flag, s, s0);
   else if (mode == kFusedLoadOnly)
-    run_fused<T, kFusedLoadOnly>(U, coef_out, zload, gather, a, flag, s, s0);
+    run_fused<T, kFusedLoadOnly>(U, coef_out, zload, gather, nullptr, a, flag, s, s0);
   else
-    run_fused<T, kFusedRecompose>(U, coef_out, zload, gather, a, flag, s, s0);
+    run_fused<T, kFusedRecompose>(U, coef_out, zload, gather, nullptr, a, flag, s, s0);
   return true;
 }
 
@@ -846,8 +873,9 @@ template std::vector<SegChoice> level_fused_candidates<double>(const LevelArgs<d
                                                                 double);
 
 template bool launch_level_fused<float>(const float*, float*, float*, float*,
-                                        const LevelArgs<float>&, int, int*, cudaStream_t, int);
+                                        const LevelArgs<float>&, int, int*, cudaStream_t, int, float*);
 template bool launch_level_fused<double>(const double*, double*, double*, double*,
-                                         const LevelArgs<double>&, int, int*, cudaStream_t, int);
+                                         const LevelArgs<double>&, int, int*, cudaStream_t, int,
+                                         double*);
 
 }  // namespace hgrb

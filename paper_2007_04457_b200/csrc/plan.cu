@@ -295,6 +295,11 @@ class PlanT final : public Plan {
   T* stage_fb_[2] = {nullptr, nullptr};
   T* const* stages_for(int l);
   T* W_ = nullptr;                     // scratch of the windowed (out-of-place) Thomas passes
+  // side rows of the top level (2D / 3D, fused): odd-column coefficients of its
+  // even rows of even planes, merged into the output with the coarser pyramid by
+  // k_merge_even (knob HGR_SIDE_ROWS=0: strided scatter instead)
+  T* E_ = nullptr;
+  bool side_used_ = false;
   // coarse tail: levels 1..tail_lt_ (all below the fused threshold, under the
   // top) run as one single-CTA launch per direction (kernels_tail.cu)
   int tail_lt_ = 0;
@@ -443,6 +448,17 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   }
   const std::size_t off_w = total;
   total += (w_n * esz + 511) & ~std::size_t(255);
+  std::size_t e_n = 0;
+  {
+    bool side = rank >= 2 && Lv >= 1 && big(Lv);
+    if (const char* v = std::getenv("HGR_SIDE_ROWS")) side = side && v[0] != '0';
+    if (side) {
+      const auto& c = ext_[std::size_t(Lv) - 1];
+      e_n = std::size_t(c[0] * c[1] * (c[2] - 1));
+    }
+  }
+  const std::size_t off_e = total;
+  total += (e_n * esz + 511) & ~std::size_t(255);
   const std::size_t off_s0 = total;
   total += (stage_n[0] * esz + 511) & ~std::size_t(255);
   const std::size_t off_s1 = total;
@@ -459,6 +475,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   for (int l = 1; l < Lv; ++l) D_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_d[std::size_t(l)]);
   for (int l = 1; l <= Lv; ++l) Z_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_z[std::size_t(l)]);
   if (w_n) W_ = reinterpret_cast<T*>(ws_ + off_w);
+  if (e_n) E_ = reinterpret_cast<T*>(ws_ + off_e);
   stage_[0] = reinterpret_cast<T*>(ws_ + off_s0);
   {
     // one CTA is the better engine only while a level is a few thousand nodes
@@ -634,9 +651,11 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
     if (!in_place) {
       // read the level once, write the coefficients and the load vector once
       prof_begin(kKindFusedDec, sz() * (n + (n - c) + c), s);
+      T* side = top ? E_ : nullptr;
       const bool ok = launch_level_fused<T>(src, coef_dst, z, nullptr, a, kFusedDecompose,
-                                            top ? d_flag_ : nullptr, s, s0_dec_[std::size_t(l)]);
+                                            top ? d_flag_ : nullptr, s, s0_dec_[std::size_t(l)], side);
       prof_end(s);
+      if (top) side_used_ = ok && side != nullptr;
       if (ok) {
         ++launch_count_;
         thomas_all(l, z, Cn, s);  // C_{l-1} = M_c^-1 K U = coarse + z
@@ -682,9 +701,12 @@ template <class T>
 void PlanT<T>::assemble(T* out, cudaStream_t s) {
   const int Lv = L();
   for (int l = 1; l <= Lv; ++l) {
+    const T* src = l == 1 ? C_[0] : D_[std::size_t(l) - 1];
     prof_begin(kKindAssembly, sz() * 2.0 * double(h.node_count(l - 1)), s);
-    launch_scatter_even<T>(l == 1 ? C_[0] : D_[std::size_t(l) - 1], l == Lv ? out : D_[std::size_t(l)],
-                           args_[std::size_t(l)], s);
+    if (l == Lv && side_used_)
+      launch_merge_even<T>(src, E_, out, args_[std::size_t(l)], s);
+    else
+      launch_scatter_even<T>(src, l == Lv ? out : D_[std::size_t(l)], args_[std::size_t(l)], s);
     prof_end(s);
     ++launch_count_;
   }
@@ -719,6 +741,7 @@ void PlanT<T>::decompose_to_direct(const void* d_in, void* d_out, cudaStream_t s
   const T* in = static_cast<const T*>(d_in);
   T* out = static_cast<T*>(d_out);
   launch_count_ = 0;
+  side_used_ = false;
   HGR_CUDA_CHECK(cudaMemsetAsync(d_flag_, 0, sizeof(int), s));
   const int Lv = L();
   if (Lv == 0) {
@@ -747,6 +770,7 @@ void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
     last_launches_[0] = launch_count_;
     return;
   }
+  side_used_ = false;
   decompose_level(Lv, data, data, true, s);
   for (int l = Lv - 1; l > tail_lt_; --l)
     decompose_level(l, C_[std::size_t(l)], D_[std::size_t(l)], false, s);
