@@ -551,13 +551,17 @@ void launch_gather(const T* src, const int64_t se[3], int64_t stride, T* dst,
              dst, de[0], de[1], de[2]);
 }
 template <class T>
+bool merge_even_fits(int64_t c2) {
+  return MergeCfg<T>::smem(c2) <= 200 * 1024;
+}
+template <class T>
 void launch_merge_even(const T* coarse, const T* side, T* out, const LevelArgs<T>& a,
                        cudaStream_t s) {
   constexpr int64_t V = MergeCfg<T>::V;
   const int64_t nvec = (a.e[2] + 2 * V - 2) / V;
   const int threads = int(std::min<int64_t>(1024, (nvec + 31) / 32 * 32));
   const size_t smem = MergeCfg<T>::smem(a.c[2]);
-  require(smem <= 200 * 1024, "merge_even: rows too long for the shared-memory ring");
+  require(merge_even_fits<T>(a.c[2]), "merge_even: rows too long for the shared-memory ring");
   set_smem_attr(reinterpret_cast<const void*>(k_merge_even<T>), smem);
   int per_sm = 0;
   HGR_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_even<T>, threads, smem));
@@ -628,6 +632,7 @@ void launch_fiber_thomas(const T* v, T* out, int64_t n, int64_t count, const T* 
                                  cudaStream_t);                                              \
   template void launch_scatter_even<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);     \
   template void launch_merge_even<T>(const T*, const T*, T*, const LevelArgs<T>&, cudaStream_t); \
+  template bool merge_even_fits<T>(int64_t);                                                 \
   template void launch_coefficients<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);     \
   template void launch_interpolate<T>(const T*, T*, const LevelArgs<T>&, cudaStream_t);      \
   template void launch_check_coarse_zero<T>(const T*, const LevelArgs<T>&, int*, cudaStream_t); \

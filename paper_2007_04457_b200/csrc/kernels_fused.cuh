@@ -77,6 +77,9 @@ bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const Leve
 // even plane of `out` (level-l extents e) is written whole, its even columns
 // from the finished level-(l-1) pyramid `coarse` (compact c) and its odd
 // columns from the side rows -- full-sector writes instead of a strided scatter.
+// whether k_merge_even's shared-memory ring holds rows of c2 coarse columns
+template <class T>
+bool merge_even_fits(int64_t c2);
 template <class T>
 void launch_merge_even(const T* coarse, const T* side, T* out, const LevelArgs<T>& a,
                        cudaStream_t s);

@@ -450,7 +450,8 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   total += (w_n * esz + 511) & ~std::size_t(255);
   std::size_t e_n = 0;
   {
-    bool side = rank >= 2 && Lv >= 1 && big(Lv);
+    // rows longer than the merge kernel's shared-memory ring keep the scatter
+    bool side = rank >= 2 && Lv >= 1 && big(Lv) && merge_even_fits<T>(ext_[std::size_t(Lv) - 1][2]);
     if (const char* v = std::getenv("HGR_SIDE_ROWS")) side = side && v[0] != '0';
     if (side) {
       const auto& c = ext_[std::size_t(Lv) - 1];
