@@ -28,6 +28,16 @@ bool thomas_needs_out_of_place(const int64_t ext[3], int dim);
 // fused per dim-0 plane by thread-block clusters from src into dst (src is
 // clobbered; dst may equal src). Returns false (nothing launched) when the
 // coarse extents or operands do not fit.
+// Streaming IPK of a 3D level (kernels_stream.cu): dim 0 as column strips in
+// place on src, then (fp32) dims 1+2 on whole planes src -> dst, or (fp64) dim 1
+// strips in place and the dim-2 row kernel src -> dst. Returns the launches
+// (0: nothing launched).
+template <class T>
+bool thomas_stream_supported(const int64_t c[3]);
+template <class T>
+int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult[3],
+                          const T* const rpiv[3], const T* const upper[3], int64_t level_nodes,
+                          cudaStream_t s);
 template <class T>
 bool thomas_band_supported(const int64_t c[3]);
 template <class T>

@@ -309,6 +309,9 @@ class PlanT final : public Plan {
   // both. Default: 1 for fp32, 0 for fp64 (its 135 KB plane tiles leave one
   // single-buffered CTA per SM; measured slower than three passes)
   int band_thomas_ = sizeof(T) == 4 ? 1 : 0;
+  // 3D IPK as streaming column passes (kernels_stream.cu), ahead of the band
+  // kernels; knob HGR_THOMAS_STREAM=0 disables
+  bool stream_thomas_ = true;
   TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
   std::vector<int> s0_dec_, s0_rec_, s0_int_;
@@ -328,6 +331,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
   if (const char* v = std::getenv("HGR_AUTOTUNE")) auto_tune_pending_ = v[0] == '1';
   if (const char* v = std::getenv("HGR_THOMAS_BAND")) band_thomas_ = std::atoi(v);
+  if (const char* v = std::getenv("HGR_THOMAS_STREAM")) stream_thomas_ = v[0] != '0';
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   s0_dec_.assign(std::size_t(h.L) + 1, 0);
   s0_rec_.assign(std::size_t(h.L) + 1, 0);
@@ -609,6 +613,17 @@ template <class T>
 void PlanT<T>::thomas_all(int l, T* src, T* last_out, cudaStream_t s) {
   const LevelArgs<T>& a = args_[std::size_t(l)];
   const int64_t c[3] = {a.c[0], a.c[1], a.c[2]};
+  if (h.rank == 3 && stream_thomas_) {
+    // dim 0 strips in place, then dims 1+2 (fp32 planes; fp64 strips + rows) into last_out
+    prof_begin(kKindThomas, sz() * (sizeof(T) == 8 ? 6.0 : 4.0) * double(c[0] * c[1] * c[2]), s);
+    const int nl = launch_thomas_stream<T>(src, last_out, c, a.mult, a.rpiv, a.upper,
+                                           int64_t(h.node_count(l)), s);
+    prof_end(s);
+    if (nl > 0) {
+      launch_count_ += nl;
+      return;
+    }
+  }
   if (h.rank == 3 && band_thomas_) {
     // two cluster passes: dim 0 in place, dims 1 + 2 fused into last_out
     prof_begin(kKindThomas, sz() * 4.0 * double(c[0] * c[1] * c[2]), s);

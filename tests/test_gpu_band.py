@@ -9,7 +9,8 @@ row-tile class (c2 = 33, 65, 129, 257, 513) and non-uniform coordinates.
 Each decompose / recompose is compared with the oracle at north_star's
 tolerance, for both dim-0 strategies (HGR_THOMAS_BAND=1: strided-line dim 0;
 =2: cluster band pass for dim 0 too), and with the three-pass path
-(HGR_THOMAS_BAND=0) of the same build.
+(HGR_THOMAS_BAND=0) of the same build. The streaming passes that precede the
+band kernels in the plan are switched off here (HGR_THOMAS_STREAM=0).
 """
 import os
 
@@ -19,6 +20,11 @@ import pytest
 import oracle
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _no_stream(monkeypatch):
+    monkeypatch.setenv("HGR_THOMAS_STREAM", "0")
 
 
 def _hgr():
