@@ -36,8 +36,8 @@ template <class T>
 bool thomas_stream_supported(const int64_t c[3]);
 template <class T>
 int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult[3],
-                          const T* const rpiv[3], const T* const upper[3], int64_t level_nodes,
-                          cudaStream_t s);
+                         const T* const rpiv[3], const T* const upper[3], const int K[3],
+                         int64_t level_nodes, cudaStream_t s);
 template <class T>
 bool thomas_band_supported(const int64_t c[3]);
 template <class T>

@@ -85,7 +85,7 @@ __host__ __device__ inline StreamLayout stream_layout(const StreamGeo& g, int rn
   L.q0 = L.tabs + 4 * nn;
   L.rows = L.q0 + (g.nb + V - 1) / V * V;
   L.bars = L.rows + 5 * rnt;  // 16-byte aligned (every piece is a 16-byte multiple)
-  L.bytes = size_t(L.bars) * sizeof(T) + size_t(2 * kStreamSlots) * 8;
+  L.bytes = size_t(L.bars) * sizeof(T) + size_t(3 * kStreamSlots) * 8;
   return L;
 }
 
@@ -106,7 +106,7 @@ __device__ __forceinline__ void load_tab(const T* t, T (&v)[R]) {
 // NT consumer threads (one column each; ROWS: also a warp per row) plus one
 // producer warp that refills the ring: full[s] completes when slot s's bytes
 // have landed, empty[s] when every consumer warp has finished the band in it.
-template <class T, int NT, bool ROWS, int CHR>
+template <class T, int NT, bool ROWS, int CHR, bool REGH>
 __global__ void __launch_bounds__(NT + 32, 1)
     k_thomas_stream(const T* in, T* out, StreamGeo G, const T* __restrict__ mult,
                     const T* __restrict__ rpiv, const T* __restrict__ upper,
@@ -197,11 +197,16 @@ __global__ void __launch_bounds__(NT + 32, 1)
       const int ph0 = int(g0 & (V - 1));
       T* dst = base + sl * G.slot;
       if (whole) {
-        if (lane == 0) {
-          const uint32_t by = uint32_t((ph0 + B * G.ncols + V - 1) / V * V * sizeof(T));
-          ptx::mbar_arrive_expect_tx(&full[sl], by);
-          ptx::bulk_g2s(dst, in + (g0 - ph0), by, &full[sl]);
-        }
+        // one contiguous block, cut into 2 KB pieces issued by the lanes (a
+        // single large bulk copy from one thread streams far below the HBM rate)
+        constexpr uint32_t PIECE = 2048;
+        const uint32_t by = uint32_t((ph0 + B * G.ncols + V - 1) / V * V * sizeof(T));
+        if (lane == 0) ptx::mbar_arrive_expect_tx(&full[sl], by);
+        __syncwarp();
+        const char* src = reinterpret_cast<const char*>(in + (g0 - ph0));
+        for (uint32_t off = uint32_t(lane) * PIECE; off < by; off += 32 * PIECE)
+          ptx::bulk_g2s(reinterpret_cast<char*>(dst) + off, src + off, min(PIECE, by - off),
+                        &full[sl]);
       } else {
         uint32_t mine = 0;
         for (int r = lane; r < B; r += 32) {
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
 
   // ---- consumers
   T yprev = T(0);
+  T hprev[REGH ? R : 1];   // REGH: backward-local values of band b - 1
   T h0r[kStreamKMax + 1];  // h0r[k]: first backward-local value of band b - k
 #pragma unroll
   for (int k = 0; k <= kStreamKMax; ++k) h0r[k] = T(0);
@@ -328,10 +334,60 @@ __global__ void __launch_bounds__(NT + 32, 1)
       ptx::named_sync(1, NT);
     }
 
-    // ---- columns: forward with the exact carry, backward-local (kept in the
-    // slot), then finish band b - K (every remaining band at the job's end)
     if (b == 0) yprev = T(0);
     const bool last = b == nb - 1;
+    if constexpr (REGH) {
+      // ---- K = 1: the column values go to registers and the slot back to the
+      // producer at once; band b-1's backward-local values wait in registers
+      // (hprev) for the carry c_b = h0(b)
+      const bool act = tid < jb.w;
+      T x[R];
+      const T* col = S + ph0 + tid;
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = (act && r < B) ? col[r * G.SP] : T(0);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[sl]);
+      if (act) {
+        T t1[R], t2[R];
+        load_tab<T, R>(tm + s, t1);
+        T y = yprev;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          y = x[r] - t1[r] * y;  // tm = 0 past the line: y stays 0 there
+          x[r] = y;
+        }
+        yprev = y;
+        load_tab<T, R>(tu + s, t1);
+        load_tab<T, R>(tp + s, t2);
+        T h = T(0);
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+          h = (x[r] - t1[r] * h) * t2[r];  // tp = 0 past the line: h stays 0 there
+          x[r] = h;
+        }
+        if (b > 0) {  // band b-1 is full
+          load_tab<T, R>(tQ + (s - R), t1);
+          T* o = out + jb.g0 + int64_t(s - R) * G.pitch + tid;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            *o = hprev[r] + h * t1[r];
+            o += G.pitch;
+          }
+        }
+        if (last) {  // the line ends here: zero carry
+          T* o = out + jb.g0 + int64_t(s) * G.pitch + tid;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (r < B) *o = x[r];
+            o += G.pitch;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) hprev[r] = x[r];
+      }
+    } else {
+    // ---- columns: forward with the exact carry, backward-local (kept in the
+    // slot), then finish band b - K (every remaining band at the job's end)
     const int nfin = last ? min(K, b) + 1 : (b >= K ? 1 : 0);
     if (tid < jb.w) {
       T* col = S + ph0 + tid;
@@ -395,6 +451,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
         }
       }
     }
+    }  // !REGH
     if (++sl == nslot) {
       sl = 0;
       ++use;
@@ -402,6 +459,278 @@ __global__ void __launch_bounds__(NT + 32, 1)
     if (last) {
       b = 0;
       if (++jl < myjobs) jb = job(jl);
+    } else {
+      ++b;
+    }
+  }
+}
+
+// Whole planes, dims 1 + 2, one lookahead band (K = 1, fp32): the row and
+// column phases of consecutive bands overlap on separate warps.
+//   producer warp     refills free slots (full[s] = bytes landed);
+//   RWN row warps     solve the band's rows along dim 2, two rows per warp, in
+//                     the slot (rows[s] = every row warp is done);
+//   CW column warps   two columns per thread (c and c + 32*CW): load the band's
+//                     column values into registers, hand the slot back
+//                     (empty[s]), solve along dim 1 and finish band b-1 from
+//                     registers with c_b = h0(b).
+// So the dim-2 solve of band b+1 runs while the dim-1 solve of band b does.
+template <class T, int CHR, int CW, int RWN>
+__global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
+    k_thomas_planes_ws(const T* in, T* out, StreamGeo G, const T* __restrict__ mult,
+                       const T* __restrict__ rpiv, const T* __restrict__ upper,
+                       const T* __restrict__ rmult, const T* __restrict__ rrpiv,
+                       const T* __restrict__ rupper) {
+  constexpr int V = int(16 / sizeof(T)), R = kStreamR, RL = 2;
+  constexpr int NTH = (CW + RWN + 1) * 32;
+  constexpr int CHRP = chunk_pitch<T, CHR>();
+  constexpr int RNT = 32 * CHRP;
+  static_assert(RL * RWN >= R, "two rows per row warp cover a band");
+  ptx::pdl_trigger();
+  extern __shared__ __align__(128) unsigned char smem_st[];
+  T* base = reinterpret_cast<T*>(smem_st);
+  const StreamLayout L = stream_layout<T>(G, RNT);
+  const int n = G.n, nb = G.nb, nslot = G.nslot;
+  T* tm = base + L.tabs;
+  const int nn = (n + V - 1) / V * V;
+  T* tu = tm + nn;
+  T* tp = tu + nn;
+  T* tQ = tp + nn;
+  T* rt = base + L.rows;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + L.bars);
+  uint64_t* rowsd = full + kStreamSlots;
+  uint64_t* empty = rowsd + kStreamSlots;
+  const int tid = threadIdx.x, lane = tid & 31, wp = ptx::warp_id_uniform();
+
+  for (int i = tid; i < nn; i += NTH) {
+    const bool in_l = i < n;
+    tm[i] = (in_l && i >= 1) ? mult[i - 1] : T(0);
+    tp[i] = in_l ? rpiv[i] : T(0);
+    tu[i] = (in_l && i < n - 1) ? upper[i] : T(0);
+    tQ[i] = T(0);
+  }
+  if (tid == 0) {
+    for (int b = 0; b < nslot; ++b) {
+      ptx::mbar_init(&full[b], 1);
+      ptx::mbar_init(&rowsd[b], RWN);
+      ptx::mbar_init(&empty[b], CW);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  for (int b = tid; b < nb; b += NTH) {
+    const int s = b * R, e = min(n, s + R);
+    T q = T(1);
+    for (int i = e - 1; i >= s; --i) {
+      q *= -(tu[i] * tp[i]);
+      tQ[i] = q;
+    }
+  }
+  build_tables(rt, rt + RNT, rt + 2 * RNT, rt + 3 * RNT, rt + 4 * RNT, G.ncols, 32, CHR, CHRP, rmult,
+               rrpiv, rupper);  // ends with __syncthreads
+
+  // jobs = planes: plane J = blockIdx.x + jl * gridDim.x, bands 0..nb-1
+  const int G0 = int(gridDim.x);
+  const int myjobs = int(blockIdx.x) < G.njobs ? (G.njobs - int(blockIdx.x) + G0 - 1) / G0 : 0;
+  const int64_t nitems = int64_t(myjobs) * nb;
+  const int P = G.ncols;  // row length == pitch == W
+  ptx::pdl_wait();  // the planes are the previous launches' output
+
+  if (wp == CW + RWN) {
+    // ---- producer: one contiguous block per band, 2 KB pieces over the lanes
+    int jl = 0, b = 0, sl = 0;
+    uint32_t use = 0;
+    for (int64_t it = 0; it < nitems; ++it) {
+      if (use > 0) ptx::mbar_wait(&empty[sl], (use - 1) & 1);
+      const int s = b * R, B = min(R, n - s);
+      const int64_t g0 = int64_t(int(blockIdx.x) + jl * G0) * G.mstride + int64_t(s) * P;
+      const int ph0 = int(g0 & (V - 1));
+      constexpr uint32_t PIECE = 2048;
+      const uint32_t by = uint32_t((ph0 + B * P + V - 1) / V * V * sizeof(T));
+      if (lane == 0) ptx::mbar_arrive_expect_tx(&full[sl], by);
+      __syncwarp();
+      const char* src = reinterpret_cast<const char*>(in + (g0 - ph0));
+      char* dst = reinterpret_cast<char*>(base + sl * G.slot);
+      for (uint32_t off = uint32_t(lane) * PIECE; off < by; off += 32 * PIECE)
+        ptx::bulk_g2s(dst + off, src + off, min(PIECE, by - off), &full[sl]);
+      if (++sl == nslot) {
+        sl = 0;
+        ++use;
+      }
+      if (++b == nb) {
+        b = 0;
+        ++jl;
+      }
+    }
+    return;
+  }
+
+  if (wp >= CW) {
+    // ---- row warps: rows 2*rw, 2*rw+1 of every band along dim 2
+    constexpr int KD = scan_depth<T, CHR>() < 31 ? scan_depth<T, CHR>() : 31;
+    const int rw = wp - CW;
+    const int q0 = lane * CHR;
+    const T* rtm = rt + lane * CHRP;
+    const T* rtP = rtm + RNT;
+    const T* rtp = rtP + RNT;
+    const T* rtu = rtp + RNT;
+    const T* rtQ = rtu + RNT;
+    const T pend = rtP[CHR - 1], qfirst = rtQ[0];
+    int jl = 0, b = 0, sl = 0;
+    uint32_t use = 0;
+    for (int64_t it = 0; it < nitems; ++it) {
+      const int s = b * R, B = min(R, n - s);
+      const int64_t g0 = int64_t(int(blockIdx.x) + jl * G0) * G.mstride + int64_t(s) * P;
+      const int ph0 = int(g0 & (V - 1));
+      T* S = base + sl * G.slot;
+      ptx::mbar_wait(&full[sl], use & 1);
+      const int r0 = RL * rw;
+      if (r0 < B) {
+        T y[RL][CHR];
+#pragma unroll
+        for (int u = 0; u < RL; ++u) {
+          const T* row = S + ph0 + (r0 + u) * P + q0;
+          const bool ok = r0 + u < B;
+#pragma unroll
+          for (int k = 0; k < CHR; ++k) y[u][k] = (ok && q0 + k < P) ? row[k] : T(0);
+        }
+        T e[RL], c[RL];
+        ChunkSolveV<T, CHR, RL>::fwd_local(y, rtm, e);
+#pragma unroll
+        for (int u = 0; u < RL; ++u) c[u] = T(0);
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+#pragma unroll
+          for (int u = 0; u < RL; ++u) {
+            const T t = __shfl_up_sync(0xffffffffu, e[u] + pend * c[u], 1);
+            c[u] = lane == 0 ? T(0) : t;
+          }
+        }
+        ChunkSolveV<T, CHR, RL>::apply(y, rtP, c);
+        ChunkSolveV<T, CHR, RL>::bwd_local(y, rtu, rtp, e);
+#pragma unroll
+        for (int u = 0; u < RL; ++u) c[u] = T(0);
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+#pragma unroll
+          for (int u = 0; u < RL; ++u) {
+            const T t = __shfl_down_sync(0xffffffffu, e[u] + qfirst * c[u], 1);
+            c[u] = lane == 31 ? T(0) : t;
+          }
+        }
+        ChunkSolveV<T, CHR, RL>::apply(y, rtQ, c);
+#pragma unroll
+        for (int u = 0; u < RL; ++u) {
+          T* row = S + ph0 + (r0 + u) * P + q0;
+          if (r0 + u < B) {
+#pragma unroll
+            for (int k = 0; k < CHR; ++k)
+              if (q0 + k < P) row[k] = y[u][k];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&rowsd[sl]);
+      if (++sl == nslot) {
+        sl = 0;
+        ++use;
+      }
+      if (++b == nb) {
+        b = 0;
+        ++jl;
+      }
+    }
+    return;
+  }
+
+  // ---- column warps: columns tid and tid + 32*CW
+  constexpr int CPT = 2;
+  T yprev[CPT], hprev[CPT][R];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) yprev[u] = T(0);
+  int jl = 0, b = 0, sl = 0;
+  uint32_t use = 0;
+  for (int64_t it = 0; it < nitems; ++it) {
+    const int s = b * R, B = min(R, n - s);
+    const int64_t gj = int64_t(int(blockIdx.x) + jl * G0) * G.mstride;
+    const int64_t g0 = gj + int64_t(s) * P;
+    const int ph0 = int(g0 & (V - 1));
+    const T* S = base + sl * G.slot + ph0;
+    const bool last = b == nb - 1;
+    ptx::mbar_wait(&rowsd[sl], use & 1);
+    T x[CPT][R];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      const int c = tid + u * 32 * CW;
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[u][r] = (c < P && r < B) ? S[r * P + c] : T(0);
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[sl]);
+    if (b == 0) {
+#pragma unroll
+      for (int u = 0; u < CPT; ++u) yprev[u] = T(0);
+    }
+    T t1[R], t2[R];
+    load_tab<T, R>(tm + s, t1);
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      T y = yprev[u];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        y = x[u][r] - t1[r] * y;  // tm = 0 past the line: y stays 0 there
+        x[u][r] = y;
+      }
+      yprev[u] = y;
+    }
+    load_tab<T, R>(tu + s, t1);
+    load_tab<T, R>(tp + s, t2);
+    T h0[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      T h = T(0);
+#pragma unroll
+      for (int r = R - 1; r >= 0; --r) {
+        h = (x[u][r] - t1[r] * h) * t2[r];  // tp = 0 past the line: h stays 0 there
+        x[u][r] = h;
+      }
+      h0[u] = h;
+    }
+    if (b > 0) {  // finish band b-1 (full) with c_b = h0(b)
+      load_tab<T, R>(tQ + (s - R), t1);
+#pragma unroll
+      for (int u = 0; u < CPT; ++u) {
+        const int c = tid + u * 32 * CW;
+        if (c < P) {
+          T* o = out + gj + int64_t(s - R) * P + c;
+#pragma unroll
+          for (int r = 0; r < R; ++r) o[r * P] = hprev[u][r] + h0[u] * t1[r];
+        }
+      }
+    }
+    if (last) {  // the plane ends here: zero carry
+#pragma unroll
+      for (int u = 0; u < CPT; ++u) {
+        const int c = tid + u * 32 * CW;
+        if (c < P) {
+          T* o = out + g0 + c;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r < B) o[r * P] = x[u][r];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CPT; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) hprev[u][r] = x[u][r];
+    if (++sl == nslot) {
+      sl = 0;
+      ++use;
+    }
+    if (last) {
+      b = 0;
+      ++jl;
     } else {
       ++b;
     }
@@ -424,12 +753,13 @@ constexpr size_t kStreamSmem = 220 * 1024;
 
 // Fill the ring geometry for a job width W; false if the tables and K + 1
 // slots do not fit.
-template <class T, int RNT>
+template <class T, int RNT, bool REGH>
 bool stream_ring(StreamGeo& g) {
   constexpr int V = int(16 / sizeof(T));
   g.nb = (g.n + kStreamR - 1) / kStreamR;
-  const int kb = (sbits<T>() + kStreamR - 1) / kStreamR;
-  g.K = std::min(kb, g.nb - 1);
+  // g.K: the plan's lookahead (tables.hpp stream_lookahead), at most nb - 1
+  g.K = std::max(1, std::min(g.K, g.nb - 1));
+  if (g.K > kStreamKMax) return false;
   const bool whole = g.W == g.ncols && int64_t(g.ncols) == g.pitch;
   if (whole) {
     g.SP = g.ncols;
@@ -445,10 +775,18 @@ bool stream_ring(StreamGeo& g) {
   const StreamLayout L1 = stream_layout<T>(g, RNT);
   const size_t fixed = L1.bytes - size_t(g.slot) * sizeof(T);
   const size_t per = size_t(g.slot) * sizeof(T);
-  if (fixed + per * size_t(g.K + 1) > kStreamSmem) return false;
+  const int held = REGH ? 0 : g.K;  // slots of unfinished bands
+  if (fixed + per * size_t(held + 3) > kStreamSmem) return false;
   const int fit = int((kStreamSmem - fixed) / per);
   g.nslot = std::min(kStreamSlots, fit);
-  return g.nslot >= g.K + 2;  // at least two bands in flight beyond the unfinished ones
+  // more bands in flight than the current one plus two measured slower (A/B at
+  // 1025^3 fp32, tools/ab_stream.sh); knob HGR_STREAM_SLOTS caps the ring
+  static const int cap = [] {
+    const char* v = std::getenv("HGR_STREAM_SLOTS");
+    return v ? std::atoi(v) : 0;
+  }();
+  g.nslot = std::min(g.nslot, cap > 0 ? cap : held + 3);
+  return g.nslot >= held + 3;  // the current band and two in flight at least
 }
 
 template <class T, int NT, bool ROWS, int CHR>
@@ -456,13 +794,35 @@ bool run_stream(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, 
                 const T* rmult, const T* rrpiv, const T* rupper, int64_t level_nodes,
                 cudaStream_t s) {
   constexpr int RNT = ROWS ? 32 * chunk_pitch<T, CHR>() : 0;
-  if (!stream_ring<T, RNT>(g)) return false;
+  auto go = [&](auto regh_c) {
+    constexpr bool REGH = decltype(regh_c)::value;
+    if (!stream_ring<T, RNT, REGH>(g)) return false;
+    const size_t smem = stream_layout<T>(g, RNT).bytes;
+    auto kern = k_thomas_stream<T, NT, ROWS, CHR, REGH>;
+    set_smem_attr(reinterpret_cast<const void*>(kern), smem);
+    const int grid = std::min(g.njobs, stream_sm_count());
+    launch_pdl(kern, dim3(unsigned(grid)), dim3(NT + 32), smem, s, level_nodes, in, out, g, mult,
+               rpiv, upper, rmult, rrpiv, rupper);
+    return true;
+  };
+  // fp32 with one lookahead band: the pending band lives in registers
+  if (sizeof(T) == 4 && std::min(g.K, g.nb - 1) <= 1) return go(std::true_type{});
+  return go(std::false_type{});
+}
+
+template <class T, int CHR, int CW, int RWN>
+bool run_planes_ws(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, const T* upper,
+                   const T* rmult, const T* rrpiv, const T* rupper, int64_t level_nodes,
+                   cudaStream_t s) {
+  constexpr int RNT = 32 * chunk_pitch<T, CHR>();
+  if (g.ncols > 2 * 32 * CW || g.ncols > 32 * CHR) return false;
+  if (!stream_ring<T, RNT, true>(g)) return false;
   const size_t smem = stream_layout<T>(g, RNT).bytes;
-  auto kern = k_thomas_stream<T, NT, ROWS, CHR>;
+  auto kern = k_thomas_planes_ws<T, CHR, CW, RWN>;
   set_smem_attr(reinterpret_cast<const void*>(kern), smem);
   const int grid = std::min(g.njobs, stream_sm_count());
-  launch_pdl(kern, dim3(unsigned(grid)), dim3(NT + 32), smem, s, level_nodes, in, out, g, mult, rpiv,
-             upper, rmult, rrpiv, rupper);
+  launch_pdl(kern, dim3(unsigned(grid)), dim3((CW + RWN + 1) * 32), smem, s, level_nodes, in, out, g,
+             mult, rpiv, upper, rmult, rrpiv, rupper);
   return true;
 }
 
@@ -471,7 +831,7 @@ bool run_stream(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, 
 // columns, at most NT).
 template <class T, int NT>
 bool stream_strips(const T* in, T* out, int n, int64_t pitch, int64_t ncols, int64_t nmat,
-                   int64_t mstride, const T* mult, const T* rpiv, const T* upper,
+                   int64_t mstride, int K, const T* mult, const T* rpiv, const T* upper,
                    int64_t level_nodes, cudaStream_t s) {
   if (ncols > (int64_t(1) << 30) || nmat * ncols > (int64_t(1) << 30)) return false;
   const int64_t sms = stream_sm_count();
@@ -494,6 +854,7 @@ bool stream_strips(const T* in, T* out, int n, int64_t pitch, int64_t ncols, int
   g.njobs = int(nmat * jpm);
   g.pitch = pitch;
   g.mstride = mstride;
+  g.K = K;
   return run_stream<T, NT, false, 1>(in, out, g, mult, rpiv, upper, nullptr, nullptr, nullptr,
                                      level_nodes, s);
 }
@@ -519,13 +880,13 @@ bool thomas_stream_supported(const int64_t c[3]) {
 
 template <class T>
 int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult[3],
-                         const T* const rpiv[3], const T* const upper[3], int64_t level_nodes,
-                         cudaStream_t s) {
+                         const T* const rpiv[3], const T* const upper[3], const int K[3],
+                         int64_t level_nodes, cudaStream_t s) {
   if (!thomas_stream_supported<T>(c)) return 0;
   if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return 0;
   constexpr bool F64 = sizeof(T) == 8;
   const int64_t plane = c[1] * c[2];
-  if (!stream_strips<T, F64 ? 256 : 512>(src, src, int(c[0]), plane, plane, 1, 0, mult[0], rpiv[0],
+  if (!stream_strips<T, F64 ? 256 : 512>(src, src, int(c[0]), plane, plane, 1, 0, K[0], mult[0], rpiv[0],
                                          upper[0], level_nodes, s))
     return 0;
   // fp32 planes whole (ROWS) by default; knob HGR_STREAM_PLANES=0: dim-1 strips
@@ -535,7 +896,7 @@ int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult
     return !v || v[0] != '0';
   }();
   if (F64 || !planes) {
-    require(stream_strips<T, F64 ? 256 : 512>(src, src, int(c[1]), c[2], c[2], c[0], plane, mult[1], rpiv[1],
+    require(stream_strips<T, F64 ? 256 : 512>(src, src, int(c[1]), c[2], c[2], c[0], plane, K[1], mult[1], rpiv[1],
                                   upper[1], level_nodes, s),
             "thomas stream: dim-1 strips do not fit after the dim-0 pass ran");
     require(launch_thomas_fast<T>(src, dst, c, 2, mult[2], rpiv[2], upper[2], s),
@@ -550,8 +911,23 @@ int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult
     g.njobs = int(c[0]);
     g.pitch = c[2];
     g.mstride = plane;
+    g.K = K[1];
     bool ok = false;
-    if (c[2] <= 32 * 5) ok = run_stream<T, 160, true, 5>(src, dst, g, mult[1], rpiv[1], upper[1],
+    static const bool ws = [] {  // knob HGR_STREAM_WS=0: one warp set for both phases
+      const char* v = std::getenv("HGR_STREAM_WS");
+      return !v || v[0] != '0';
+    }();
+    if (ws && std::min(g.K, int((c[1] + kStreamR - 1) / kStreamR) - 1) <= 1) {
+#define HGR_WS(CHR, CW)                                                                          \
+  run_planes_ws<T, CHR, CW, 8>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2], upper[2], \
+                               level_nodes, s)
+      if (c[2] <= 32 * 5) ok = HGR_WS(5, 3);
+      else if (c[2] <= 32 * 9) ok = HGR_WS(9, 5);
+      else ok = HGR_WS(17, 9);
+#undef HGR_WS
+    }
+    if (ok) {
+    } else if (c[2] <= 32 * 5) ok = run_stream<T, 160, true, 5>(src, dst, g, mult[1], rpiv[1], upper[1],
                                                          mult[2], rpiv[2], upper[2], level_nodes, s);
     else if (c[2] <= 32 * 9) ok = run_stream<T, 288, true, 9>(src, dst, g, mult[1], rpiv[1], upper[1],
                                                               mult[2], rpiv[2], upper[2], level_nodes, s);
@@ -565,10 +941,10 @@ int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult
 template bool thomas_stream_supported<float>(const int64_t*);
 template bool thomas_stream_supported<double>(const int64_t*);
 template int launch_thomas_stream<float>(float*, float*, const int64_t*, const float* const*,
-                                         const float* const*, const float* const*, int64_t,
-                                         cudaStream_t);
+                                         const float* const*, const float* const*, const int*,
+                                         int64_t, cudaStream_t);
 template int launch_thomas_stream<double>(double*, double*, const int64_t*, const double* const*,
-                                           const double* const*, const double* const*, int64_t,
-                                           cudaStream_t);
+                                           const double* const*, const double* const*, const int*,
+                                           int64_t, cudaStream_t);
 
 }  // namespace hgrb

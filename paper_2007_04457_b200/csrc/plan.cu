@@ -285,6 +285,8 @@ class PlanT final : public Plan {
 
   std::vector<LevelArgs<T>> args_;     // index l = 1..L (0 unused)
   std::vector<std::array<int64_t, 3>> ext_;  // canonical extents per level 0..L
+  // lookahead bands of the streaming IPK passes per (level, canonical dim)
+  std::vector<std::array<int, 3>> stream_k_;
   std::vector<T*> C_;                  // compact level arrays 0..L-1
   std::vector<T*> D_;                  // compact coefficient arrays 1..L-1 (decompose)
   std::vector<T*> Z_;                  // corrections 1..L
@@ -353,6 +355,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
     std::size_t wl, wr, taps, mult, pivot, upper, rpiv, h, trl, trr;
   };
   std::vector<std::array<Off, 3>> offs(std::size_t(Lv) + 1);
+  stream_k_.assign(std::size_t(Lv) + 1, std::array<int, 3>{0, 0, 0});
   for (int l = 1; l <= Lv; ++l) {
     for (int d = 0; d < rank; ++d) {
       const int k = d + 3 - rank;
@@ -382,6 +385,10 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
       o.pivot = push(pivot);
       o.upper = push(upper);
       o.rpiv = push(rpiv);
+      stream_k_[std::size_t(l)][std::size_t(k)] = stream_lookahead<T>(upper, rpiv);
+      if (const char* v = std::getenv("HGR_STREAM_K"))  // test knob: at least this many
+        stream_k_[std::size_t(l)][std::size_t(k)] =
+            std::max(stream_k_[std::size_t(l)][std::size_t(k)], std::atoi(v));
       offs[std::size_t(l)][std::size_t(k)] = o;
     }
   }
@@ -617,6 +624,7 @@ void PlanT<T>::thomas_all(int l, T* src, T* last_out, cudaStream_t s) {
     // dim 0 strips in place, then dims 1+2 (fp32 planes; fp64 strips + rows) into last_out
     prof_begin(kKindThomas, sz() * (sizeof(T) == 8 ? 6.0 : 4.0) * double(c[0] * c[1] * c[2]), s);
     const int nl = launch_thomas_stream<T>(src, last_out, c, a.mult, a.rpiv, a.upper,
+                                           stream_k_[std::size_t(l)].data(),
                                            int64_t(h.node_count(l)), s);
     prof_end(s);
     if (nl > 0) {

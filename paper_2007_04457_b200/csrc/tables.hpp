@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstddef>
+#include <cmath>
 #include <vector>
 
 namespace hgrb {
@@ -74,6 +75,35 @@ inline void thomas_factors(const std::vector<T>& h, std::vector<T>& mult, std::v
     pivot[i] = main_(i) - mult[i - 1] * upper[i - 1];
   }
   for (std::size_t i = 0; i < n; ++i) rpiv[i] = T(1) / pivot[i];
+}
+
+// Lookahead bands of the streaming IPK passes (kernels_stream.cu, bands of
+// kStreamBand positions): the smallest K such that the backward carry through
+// any K consecutive bands -- the product of the factors u_i / p_i over their
+// positions -- is below 2^-bits (56 fp64, 26 fp32), i.e. below rounding. The
+// bound 1/2 per factor gives K = ceil(bits / 16); the actual factors of a grid
+// (about 0.27 on uniform spacings) usually give less. Returns at least 1.
+constexpr int kStreamBand = 16;
+template <class T>
+inline int stream_lookahead(const std::vector<T>& upper, const std::vector<T>& rpiv) {
+  const double bits = sizeof(T) == 8 ? 56.0 : 26.0;
+  const std::size_t n = rpiv.size();
+  const std::size_t nb = (n + kStreamBand - 1) / kStreamBand;
+  std::vector<double> d(nb, 0.0);  // -log2 of each band's carry factor
+  for (std::size_t i = 0; i < n; ++i) {
+    const double f = i + 1 < n ? std::fabs(double(upper[i]) * double(rpiv[i])) : 0.0;
+    d[i / kStreamBand] += f > 0.0 ? -std::log2(f) : 1e300;
+  }
+  for (std::size_t K = 1; K + 1 < nb; ++K) {
+    bool ok = true;
+    for (std::size_t b = 1; b + K <= nb && ok; ++b) {  // bands b .. b+K-1 after a finished one
+      double s = 0.0;
+      for (std::size_t t = 0; t < K; ++t) s += d[b + t];
+      ok = s >= bits;
+    }
+    if (ok) return int(K);
+  }
+  return int(nb > 1 ? nb - 1 : 1);
 }
 
 // Transfer weights in T (refined_node_weights<T>, correction.hpp:67-88): the

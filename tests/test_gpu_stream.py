@@ -47,6 +47,20 @@ def _ids(c):
         ("_nu" if c[2] else "")
 
 
+# lookahead forced up (HGR_STREAM_K): fp32 levels whose uniform spacings need one
+# lookahead band otherwise take the shared-memory path of the pending bands
+FORCED_K = [((257, 257, 257), np.float32, False), ((33, 1025, 513), np.float32, True),
+            ((129, 129, 129), np.float64, False)]
+
+
+@pytest.mark.parametrize("shape,dt,nonuniform", FORCED_K, ids=[_ids(c) for c in FORCED_K])
+@pytest.mark.parametrize("k", ["2", "4"])
+def test_stream_thomas_forced_lookahead(cuda, port, parity_log, monkeypatch, shape, dt,
+                                        nonuniform, k):
+    monkeypatch.setenv("HGR_STREAM_K", k)
+    test_stream_thomas_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform)
+
+
 @pytest.mark.parametrize("shape,dt,nonuniform", CASES, ids=[_ids(c) for c in CASES])
 def test_stream_thomas_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform):
     import torch
