@@ -71,7 +71,8 @@ struct StreamGeo {
 };
 
 // shared-memory layout (in T units from the base): slots | tm tu tp tQ (n each,
-// rounded to 16 bytes) | q0 (nb) | row tables (ROWS) | mbarriers
+// rounded up to whole bands and zero past the line) | q0 (nb) | row tables
+// (ROWS) | mbarriers
 struct StreamLayout {
   int tabs, q0, rows, bars;
   size_t bytes;
@@ -81,7 +82,8 @@ __host__ __device__ inline StreamLayout stream_layout(const StreamGeo& g, int rn
   constexpr int V = int(16 / sizeof(T));
   StreamLayout L;
   L.tabs = g.nslot * g.slot;
-  const int nn = (g.n + V - 1) / V * V;
+  // whole bands: a band's 16-entry table loads stay inside its own (zeroed) table
+  const int nn = (g.n + kStreamR - 1) / kStreamR * kStreamR;
   L.q0 = L.tabs + 4 * nn;
   L.rows = L.q0 + (g.nb + V - 1) / V * V;
   L.bars = L.rows + 5 * rnt;  // 16-byte aligned (every piece is a 16-byte multiple)
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
   const StreamLayout L = stream_layout<T>(G, RNT);
   const int n = G.n, nb = G.nb, K = G.K, nslot = G.nslot;
   T* tm = base + L.tabs;
-  const int nn = (n + V - 1) / V * V;
+  const int nn = (n + R - 1) / R * R;  // whole bands (stream_layout)
   T* tu = tm + nn;
   T* tp = tu + nn;
   T* tQ = tp + nn;
@@ -492,7 +494,7 @@ __global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
   const StreamLayout L = stream_layout<T>(G, RNT);
   const int n = G.n, nb = G.nb, nslot = G.nslot;
   T* tm = base + L.tabs;
-  const int nn = (n + V - 1) / V * V;
+  const int nn = (n + R - 1) / R * R;  // whole bands (stream_layout)
   T* tu = tm + nn;
   T* tp = tu + nn;
   T* tQ = tp + nn;
