@@ -8,8 +8,8 @@ CLASSES = {  # bench kind -> (kernel-name regex, bench brackets per round trip)
     "fused_decompose_level": (r"k_level_(fused|face)<\w+, 0>", None),
     "fused_recompose_level": (r"k_level_(fused|face)<\w+, 2>", None),
     "recompose_interp": (r"k_interp_(march|face)", None),
-    "thomas": (r"k_thomas_(lines|rows|long)", None),
-    "assembly": (r"k_scatter_even", None),
+    "thomas": (r"k_thomas_(lines|rows|long|stream|planes_ws|band)", None),
+    "assembly": (r"k_(scatter|merge)_even", None),
     "small_levels": (r"k_(tail_\w+|lpk|thomas|coefficients|gather|gpk_dec|gpk_rec|axpy|check_finite)<", None),
 }
 
