@@ -30,6 +30,7 @@
 //   loads in flight (Little's law at ~44 GB/s per SM) while the consumer warps,
 //   each column independent of the others, compute without CTA barriers.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -477,8 +478,17 @@ __global__ void __launch_bounds__(NT + 32, 1)
 //                     (empty[s]), solve along dim 1 and finish band b-1 from
 //                     registers with c_b = h0(b).
 // So the dim-2 solve of band b+1 runs while the dim-1 solve of band b does.
-template <class T, int CHR, int CW, int RWN>
-__global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
+// registers per thread for one CTA per SM: the warps are spread over the four
+// SM sub-partitions, each with a 16K-register file, so the busiest one holds
+// ceil(warps / 4) warps (launch bounds alone let ptxas stop below this)
+constexpr int ws_maxnreg(int nth) {
+  return (16384 / (((nth / 32) + 3) / 4 * 32)) / 8 * 8 > 255
+             ? 255
+             : (16384 / (((nth / 32) + 3) / 4 * 32)) / 8 * 8;
+}
+
+template <class T, int CHR, int CW, int RWN, bool PROV>
+__global__ void __maxnreg__(ws_maxnreg((CW + RWN + 1) * 32))
     k_thomas_planes_ws(const T* in, T* out, StreamGeo G, const T* __restrict__ mult,
                        const T* __restrict__ rpiv, const T* __restrict__ upper,
                        const T* __restrict__ rmult, const T* __restrict__ rrpiv,
@@ -520,6 +530,7 @@ __global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  T* q0b = base + L.q0;
   for (int b = tid; b < nb; b += NTH) {
     const int s = b * R, e = min(n, s + R);
     T q = T(1);
@@ -527,6 +538,7 @@ __global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
       q *= -(tu[i] * tp[i]);
       tQ[i] = q;
     }
+    q0b[b] = q;
   }
   build_tables(rt, rt + RNT, rt + 2 * RNT, rt + 3 * RNT, rt + 4 * RNT, G.ncols, 32, CHR, CHRP, rmult,
                rrpiv, rupper);  // ends with __syncthreads
@@ -647,7 +659,13 @@ __global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
 
   // ---- column warps: columns tid and tid + 32*CW
   constexpr int CPT = 2;
-  T yprev[CPT], hprev[CPT][R];
+  const int K = G.K;
+  T yprev[CPT], hprev[PROV ? 1 : CPT][PROV ? 1 : R];
+  T h0h[PROV ? CPT : 1][kStreamKMax + 1];  // PROV: first backward-local values of bands b-k
+#pragma unroll
+  for (int u = 0; u < (PROV ? CPT : 1); ++u)
+#pragma unroll
+    for (int k = 0; k <= kStreamKMax; ++k) h0h[u][k] = T(0);
 #pragma unroll
   for (int u = 0; u < CPT; ++u) yprev[u] = T(0);
   int jl = 0, b = 0, sl = 0;
@@ -698,6 +716,52 @@ __global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
       }
       h0[u] = h;
     }
+    if constexpr (PROV) {
+      // ---- K >= 1 pending bands without registers for them: band b goes out as
+      // provisional values (final for the plane's last band), and band b-K is
+      // corrected in place (L2-resident: written K bands ago) once c_b is known
+#pragma unroll
+      for (int u = 0; u < CPT; ++u) {
+        const int c = tid + u * 32 * CW;
+        if (c < P) {
+          T* o = out + g0 + c;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r < B) o[r * P] = x[u][r];
+        }
+#pragma unroll
+        for (int k = kStreamKMax; k >= 1; --k) h0h[u][k] = h0h[u][k - 1];
+        h0h[u][0] = h0[u];
+      }
+      auto fix = [&](int d) {  // band b-d (full): z += c_b * Q, c_b from bands b-d+1 .. b
+        const int s0 = (b - d) * R;
+        load_tab<T, R>(tQ + s0, t1);
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+          const int c = tid + u * 32 * CW;
+          T cb = T(0), coef = T(1);
+#pragma unroll
+          for (int k = kStreamKMax; k >= 0; --k)
+            if (k < d) {
+              cb += coef * h0h[u][k];
+              coef *= q0b[b - k];
+            }
+          if (c < P) {
+            T* o = out + gj + int64_t(s0) * P + c;
+            T z[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) z[r] = o[r * P];
+#pragma unroll
+            for (int r = 0; r < R; ++r) o[r * P] = z[r] + cb * t1[r];
+          }
+        }
+      };
+      if (!last) {
+        if (b >= K) fix(K);
+      } else {
+        for (int d = min(K, b); d >= 1; --d) fix(d);
+      }
+    } else {
     if (b > 0) {  // finish band b-1 (full) with c_b = h0(b)
       load_tab<T, R>(tQ + (s - R), t1);
 #pragma unroll
@@ -726,6 +790,7 @@ __global__ void __launch_bounds__((CW + RWN + 1) * 32, 1)
     for (int u = 0; u < CPT; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) hprev[u][r] = x[u][r];
+    }  // !PROV
     if (++sl == nslot) {
       sl = 0;
       ++use;
@@ -756,7 +821,7 @@ constexpr size_t kStreamSmem = 220 * 1024;
 // Fill the ring geometry for a job width W; false if the tables and K + 1
 // slots do not fit.
 template <class T, int RNT, bool REGH>
-bool stream_ring(StreamGeo& g) {
+bool stream_ring(StreamGeo& g, int min_slots = 0) {
   constexpr int V = int(16 / sizeof(T));
   g.nb = (g.n + kStreamR - 1) / kStreamR;
   // g.K: the plan's lookahead (tables.hpp stream_lookahead), at most nb - 1
@@ -778,7 +843,8 @@ bool stream_ring(StreamGeo& g) {
   const size_t fixed = L1.bytes - size_t(g.slot) * sizeof(T);
   const size_t per = size_t(g.slot) * sizeof(T);
   const int held = REGH ? 0 : g.K;  // slots of unfinished bands
-  if (fixed + per * size_t(held + 3) > kStreamSmem) return false;
+  const int need = min_slots > 0 ? min_slots : held + 3;
+  if (fixed + per * size_t(need) > kStreamSmem) return false;
   const int fit = int((kStreamSmem - fixed) / per);
   g.nslot = std::min(kStreamSlots, fit);
   // more bands in flight than the current one plus two measured slower (A/B at
@@ -789,8 +855,8 @@ bool stream_ring(StreamGeo& g) {
   }();
   // (fp32); fp64 bands of 16 rows of 256 doubles take every slot that fits (A/B
   // at 1025^3 fp64: IPK 3.05 -> 2.98 ms with 6 slots instead of 5)
-  g.nslot = std::min(g.nslot, cap > 0 ? cap : sizeof(T) == 8 ? g.nslot : held + 3);
-  return g.nslot >= held + 3;  // the current band and two in flight at least
+  g.nslot = std::min(g.nslot, cap > 0 ? cap : sizeof(T) == 8 ? g.nslot : std::max(need, held + 3));
+  return g.nslot >= need;  // by default the current band and two in flight at least
 }
 
 template <class T, int NT, bool ROWS, int CHR>
@@ -814,16 +880,32 @@ bool run_stream(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, 
   return go(std::false_type{});
 }
 
-template <class T, int CHR, int CW, int RWN>
+template <class T, int CHR, int CW, int RWN, bool PROV>
 bool run_planes_ws(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, const T* upper,
                    const T* rmult, const T* rrpiv, const T* rupper, int64_t level_nodes,
                    cudaStream_t s) {
   constexpr int RNT = 32 * chunk_pitch<T, CHR>();
   if (g.ncols > 2 * 32 * CW || g.ncols > 32 * CHR) return false;
-  if (!stream_ring<T, RNT, true>(g)) return false;
-  const size_t smem = stream_layout<T>(g, RNT).bytes;
-  auto kern = k_thomas_planes_ws<T, CHR, CW, RWN>;
-  set_smem_attr(reinterpret_cast<const void*>(kern), smem);
+  // PROV (pending bands corrected in place in global memory): two slots suffice,
+  // the column warps hand a slot back as soon as its band is in registers
+  if (!stream_ring<T, RNT, true>(g, PROV ? 2 : 0)) return false;
+  auto kern = k_thomas_planes_ws<T, CHR, CW, RWN, PROV>;
+  // the ring as deep as one resident CTA allows (shared memory + registers)
+  size_t smem = 0;
+  for (;; --g.nslot) {
+    smem = stream_layout<T>(g, RNT).bytes;
+    set_smem_attr(reinterpret_cast<const void*>(kern), smem);
+    int per_sm = 0;
+    const cudaError_t oe =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (CW + RWN + 1) * 32, smem);
+    if (oe != cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 0;
+    }
+
+    if (per_sm > 0) break;
+    if (g.nslot <= 2) return false;
+  }
   const int grid = std::min(g.njobs, stream_sm_count());
   launch_pdl(kern, dim3(unsigned(grid)), dim3((CW + RWN + 1) * 32), smem, s, level_nodes, in, out, g,
              mult, rpiv, upper, rmult, rrpiv, rupper);
@@ -899,6 +981,37 @@ int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult
     const char* v = std::getenv("HGR_STREAM_PLANES");
     return !v || v[0] != '0';
   }();
+  // fp64 dims 1 + 2 on whole planes, pending bands corrected in place in global
+  // memory (knob HGR_STREAM_PLANES64=1): two 66 KB slots only, and the
+  // corrections re-write bands L2 has partly evicted (1025^3: 853 us against
+  // 380 + 335 us for dim-1 strips + rows), so off by default
+  const bool planes64 = [] {  // read per launch: tests switch it within a process
+    const char* v = std::getenv("HGR_STREAM_PLANES64");
+    return v && v[0] == '1';
+  }();
+  if (F64 && planes && planes64) {
+    // fp64 dims 1 + 2 on whole planes: pending bands corrected in place
+    StreamGeo g{};
+    g.n = int(c[1]);
+    g.W = int(c[2]);
+    g.jpm = 1;
+    g.ncols = int(c[2]);
+    g.njobs = int(c[0]);
+    g.pitch = c[2];
+    g.mstride = plane;
+    g.K = K[1];
+    bool ok = false;
+    if (c[2] <= 32 * 5)
+      ok = run_planes_ws<T, 5, 3, 8, true>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2],
+                                           upper[2], level_nodes, s);
+    else if (c[2] <= 32 * 9)
+      ok = run_planes_ws<T, 9, 5, 8, true>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2],
+                                           upper[2], level_nodes, s);
+    else
+      ok = run_planes_ws<T, 17, 9, 8, true>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2],
+                                            upper[2], level_nodes, s);
+    if (ok) return 2;
+  }
   if (F64 || !planes) {
     require(stream_strips<T, F64 ? 256 : 512>(src, src, int(c[1]), c[2], c[2], c[0], plane, K[1], mult[1], rpiv[1],
                                   upper[1], level_nodes, s),
@@ -923,7 +1036,7 @@ int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult
     }();
     if (ws && std::min(g.K, int((c[1] + kStreamR - 1) / kStreamR) - 1) <= 1) {
 #define HGR_WS(CHR, CW)                                                                          \
-  run_planes_ws<T, CHR, CW, 8>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2], upper[2], \
+  run_planes_ws<T, CHR, CW, 8, false>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2], upper[2], \
                                level_nodes, s)
       if (c[2] <= 32 * 5) ok = HGR_WS(5, 3);
       else if (c[2] <= 32 * 9) ok = HGR_WS(9, 5);

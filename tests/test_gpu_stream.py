@@ -61,6 +61,16 @@ def test_stream_thomas_forced_lookahead(cuda, port, parity_log, monkeypatch, sha
     test_stream_thomas_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform)
 
 
+# fp64 whole-plane pass with the pending bands corrected in place (off by default)
+PLANES64 = [c for c in CASES if c[1] == np.float64]
+
+
+@pytest.mark.parametrize("shape,dt,nonuniform", PLANES64, ids=[_ids(c) for c in PLANES64])
+def test_stream_planes64_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform):
+    monkeypatch.setenv("HGR_STREAM_PLANES64", "1")
+    test_stream_thomas_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform)
+
+
 @pytest.mark.parametrize("shape,dt,nonuniform", CASES, ids=[_ids(c) for c in CASES])
 def test_stream_thomas_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform):
     import torch
