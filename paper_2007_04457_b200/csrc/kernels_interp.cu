@@ -14,7 +14,10 @@
 // row stores. Lane L of column group G owns coarse column t = 32G + L and fine
 // cells 2t, 2t+1; the warps of a group own bands of four fine rows. In-place
 // safe (every cell is read before it is written, by the CTA that owns it).
-// The last fine row and column of the level are the faces of k_interp_face.
+// The last fine row and column of the level (the faces) are written by the last
+// tile row / column: the lane whose right coarse neighbour is the last coarse
+// column computes one extra cell, the band holding the last fine row one extra
+// row, so those rows are stored whole (no strided face writes).
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
@@ -52,7 +55,7 @@ struct ICfg {
   static constexpr int BOX = (FC + V - 1 + V - 1) / V * V;     // aligned superset of a row
   static constexpr int PITCH = (BOX + ALN - 1) / ALN * ALN;
   static_assert(PITCH >= FC + V + 4, "vector reads stay inside the row");
-  static constexpr int SLOT = FR * PITCH;
+  static constexpr int SLOT = (FR + 1) * PITCH;                // + the last fine row (face)
   static constexpr int CR = TW1 + 1, CC = TW2 + 1;             // coarse window
   static constexpr int CBOX = (CC + V - 1 + V - 1) / V * V;
   static constexpr int CPITCH = (CBOX + ALN - 1) / ALN * ALN;
@@ -169,6 +172,8 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
   const int64_t kb = lastseg ? c0 - 1 : ka + S0;  // coarse planes ka..kb
   const int64_t jlo = 2 * ka, jhi = lastseg ? e0 - 1 : 2 * kb - 1;  // owned fine planes
   const int frows = 2 * tw1;
+  // faces: the last coarse column / row of the level is this tile's +1 neighbour
+  const bool xcol = c2 - 1 - q2a <= TW2, xrow = c1 - 1 - q1a <= TW1;
 
   const int grp = warp / WG, wg = warp % WG;
   const int t0 = CPL * (32 * grp + lane);  // tile-local coarse columns t0..t0+CPL-1
@@ -180,11 +185,18 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     hl[c] = cvalid[c] ? a.wl[2][q2a + t0 + c] : T(0);
     hr[c] = cvalid[c] ? a.wr[2][q2a + t0 + c] : T(0);
   }
+  // face cell of this lane (the even cell of coarse column tw2 = c2-1): index fk
+  // of its NCELL + 1 cells, or -1
+  int fk = -1;
+  if (xcol && tw2 - t0 >= 0 && tw2 - t0 <= CPL) fk = 2 * (tw2 - t0);
   const bool has_band = wg < NB;
-  const int b = 4 * wg;  // fine rows b..b+3 of the tile; coarse rows b/2 .. b/2+2
-  bool rown[4];
+  const int b = 4 * wg;  // fine rows b..b+4 of the tile; coarse rows b/2 .. b/2+2
+  // row b+4 is only ever the last fine row of a full-height last tile row
+  bool rown[5];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) rown[i] = has_band && b + i < frows;
+  for (int i = 0; i < 5; ++i)
+    rown[i] = has_band && (i < 4 ? (b + i < frows || (xrow && b + i == frows))
+                                 : (xrow && b + 4 == frows && frows == 2 * TW1));
   T w1l[2] = {T(0), T(0)}, w1r[2] = {T(0), T(0)};  // odd fine rows b+1, b+3
   if (has_band) {
 #pragma unroll
@@ -196,7 +208,8 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
 
   // ---- TMA: fine coefficient rows and coarse C / Z rows --------------------------------
   const int64_t plane_f = e1 * e2, plane_c = c1 * c2;
-  const uint32_t tx_f = uint32_t(frows) * C::BOX * uint32_t(sizeof(T));
+  const int frows_ld = frows + (xrow ? 1 : 0);  // + the last fine row
+  const uint32_t tx_f = uint32_t(frows_ld) * C::BOX * uint32_t(sizeof(T));
   const int crows = tw1 + 1;
   const uint32_t tx_c = uint32_t(crows) * C::CBOX * uint32_t(sizeof(T)) * (HASZ ? 2u : 1u);
   const uint32_t ring_s = ptx::smem_addr(ring), cbuf_s = ptx::smem_addr(cbuf);
@@ -208,7 +221,7 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
       const uint32_t dst = ring_s + uint32_t(sl * SLOT * sizeof(T));
       const uint32_t bs = barf_s + uint32_t(sl * sizeof(uint64_t));
       const int64_t base = (j * e1 + 2 * q1a) * e2 + 2 * q2a - coef_off;
-      for (int r = warp; r < frows; r += NW) {
+      for (int r = warp; r < frows_ld; r += NW) {
         const int64_t f = base + int64_t(r) * e2;
         ptx::tma_load_1d_s(dst + uint32_t(r * PITCH * sizeof(T)), &mcoef, int(f & ~int64_t(V - 1)), bs);
       }
@@ -264,11 +277,12 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     return int((m * plane_c + cph0 + int64_t(s) * c2m) & (V - 1)) + t0;
   };
 
-  T A1p[4][NCELL], A1[4][NCELL];
+  constexpr int NC1 = NCELL + 1;  // + the face cell
+  T A1p[5][NC1], A1[5][NC1];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 5; ++i)
 #pragma unroll
-    for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[i][k] = T(0);
+    for (int k = 0; k < NC1; ++k) A1p[i][k] = A1[i][k] = T(0);
   T* obase = out + (2 * q1a + b) * e2 + 2 * q2a + 2 * t0;
 
   // one fine plane j: out = coef + interp (interp alone at coarse nodes / without coef)
@@ -281,29 +295,43 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     // one row; PH: the phase of the row's cells (compile time), or -1
     auto row = [&](auto i_c, auto ph_c) {
       constexpr int i = decltype(i_c)::value, PH = decltype(ph_c)::value;
-      T v[NCELL];
+      if (i == 4 && !rown[4]) return;
+      T v[NC1];
 #pragma unroll
-      for (int k = 0; k < NCELL; ++k) v[k] = odd ? w0l * A1p[i][k] + w0r * A1[i][k] : A1[i][k];
+      for (int k = 0; k < NC1; ++k) v[k] = odd ? w0l * A1p[i][k] + w0r * A1[i][k] : A1[i][k];
       if (WITH) {
-        T cf[NCELL];
-        if constexpr (PH >= 0) ldnc<T, NCELL, PH>(S + (b + i) * PITCH, fpos(j, b + i), cf);
-        else ldn<T, NCELL>(S + (b + i) * PITCH, fpos(j, b + i), cf);
+        T cf[NC1];
+        {
+          T c4[NCELL];
+          const T* rowp = S + (b + i) * PITCH;
+          const int pos = fpos(j, b + i);
+          if constexpr (PH >= 0) ldnc<T, NCELL, PH>(rowp, pos, c4);
+          else ldn<T, NCELL>(rowp, pos, c4);
 #pragma unroll
-        for (int k = 0; k < NCELL; ++k)
+          for (int k = 0; k < NCELL; ++k) cf[k] = c4[k];
+          cf[NCELL] = fk == NCELL ? rowp[pos + NCELL] : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < NC1; ++k)
           // the coarse nodes (even plane, even row, even column) keep the interpolant
           if (odd || (i & 1) || (k & 1)) v[k] += cf[k];
       }
       if (rown[i]) {
+        T* orow = o + int64_t(i) * e2;
+        if (fk == NCELL) orow[NCELL] = v[NCELL];
         // the output has the coefficients' layout: same phase when both are aligned
         if constexpr (PH >= 0) {
           if (vstore) {
-            store_cells<T, NCELL, PH>(o + int64_t(i) * e2, v);
+            T v4[NCELL];
+#pragma unroll
+            for (int k = 0; k < NCELL; ++k) v4[k] = v[k];
+            store_cells<T, NCELL, PH>(orow, v4);
             return;
           }
         }
 #pragma unroll
         for (int k = 0; k < NCELL; ++k)
-          if (cvalid[k >> 1]) o[int64_t(i) * e2 + k] = v[k];
+          if (cvalid[k >> 1] || k == fk) orow[k] = v[k];
       }
     };
     auto rows4 = [&](auto phb_c) {
@@ -313,6 +341,7 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
       row(IC<1>{}, ph(IC<1>{}));
       row(IC<2>{}, ph(IC<2>{}));
       row(IC<3>{}, ph(IC<3>{}));
+      row(IC<4>{}, ph(IC<4>{}));
     };
     if (ph_regular) {
       const int phb = fpos(j, b) & (V - 1);
@@ -338,7 +367,7 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     ptx::mbar_wait(&barc[bsl], uint32_t(((m - ka) >> 1) & 1));
     if (has_band) {
       const T* Cb = cbuf + bsl * 2 * CSLOT;
-      T A2[3][NCELL];
+      T A2[3][NC1];
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const int s = b / 2 + k;
@@ -356,13 +385,15 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
           A2[k][2 * c] = x[c];
           A2[k][2 * c + 1] = hl[c] * x[c] + hr[c] * x[c + 1];
         }
+        A2[k][NCELL] = x[CPL];  // the face cell (coarse column t0 + CPL)
       }
 #pragma unroll
-      for (int c = 0; c < NCELL; ++c) {
+      for (int c = 0; c < NC1; ++c) {
         A1[0][c] = A2[0][c];
         A1[1][c] = w1l[0] * A2[0][c] + w1r[0] * A2[1][c];
         A1[2][c] = A2[1][c];
         A1[3][c] = w1l[1] * A2[1][c] + w1r[1] * A2[2][c];
+        A1[4][c] = A2[2][c];
       }
     }
     // ---- fine planes 2m-1 (odd) and 2m (even)
@@ -372,9 +403,9 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     }
     if (2 * m <= jhi) fine_plane(2 * m, false, T(0), T(0));
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 5; ++i)
 #pragma unroll
-      for (int k = 0; k < NCELL; ++k) A1p[i][k] = A1[i][k];
+      for (int k = 0; k < NC1; ++k) A1p[i][k] = A1[i][k];
     __syncthreads();  // slots of planes 2m-1, 2m and coarse buffer m are free
     if (WITH) {
       if (m > ka && 2 * m - 1 + NS <= jhi) issue_f(2 * m - 1 + NS);
@@ -484,8 +515,7 @@ bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const Leve
   else if (with) run_interp<T, true, false>(coef, out, C, Z, a, s, s0);
   else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s, s0);
   else run_interp<T, false, false>(coef, out, C, Z, a, s, s0);
-  launch_pdl(k_interp_face<T>, dim3(unsigned(a.e[0]), 2, unsigned((std::max(a.e[1], a.e[2]) + 255) / 256)), dim3(256), 0, s, a.e[0] * a.e[1] * a.e[2], coef, out, C, Z, a, with);
-  HGR_CUDA_CHECK(cudaGetLastError());
+  // the faces (last fine row / column) are written by the last tiles
   return true;
 }
 
