@@ -81,7 +81,13 @@ enum FusedMode : int {
 // rows are left for launch_merge_even.
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
-                        int mode, int* flag, cudaStream_t s, int s0 = 0, T* side = nullptr);
+                        int mode, int* flag, cudaStream_t s, int s0 = 0, T* side = nullptr,
+                        T* face_ws = nullptr);
+// face scratch of launch_level_fused's two-phase faces: e0*e1 + 3*e0*c2 elements
+template <class T>
+inline int64_t level_face_ws_elems(const int64_t e[3], const int64_t c[3]) {
+  return e[0] * e[1] + 3 * e[0] * c[2];
+}
 
 // Pyramid assembly of a level decomposed with side rows: every even row of an
 // even plane of `out` (level-l extents e) is written whole, its even columns

@@ -745,6 +745,146 @@ __global__ void __launch_bounds__(256)
   if (flag && __syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
 }
 
+// Two-phase faces (default; the scratch comes from the plan). Phase 1 reads each
+// face slab of the fine level once:
+//   blockIdx.y = 0: R2[j][r] = K2 of the last coarse column at fine row r of fine
+//       plane j (the last three fine columns; strided, one sector per row), and
+//       (decompose) the checks and coefficients of the cells on the last fine column;
+//   blockIdx.y = 1: P2f[j][y][q2] = K2 of coarse column q2 at fine row e1-3+y
+//       (contiguous rows), and (decompose) the cells on the last fine row
+//       (columns < e2-1; side rows for the odd columns of even planes).
+// Phase 2 forms the load vector on the faces from those compact arrays, K1 and K0
+// over coalesced rows (recompose: plus the gather of the face coarse nodes).
+// Recompose masks the coarse nodes (correction.hpp:251) in phase 1.
+constexpr int kFaceItems = 1024;  // phase-1 items per CTA (4 per thread)
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(256)
+    k_face_slab(const T* __restrict__ U, T* __restrict__ coef_out, T* __restrict__ side,
+                T* __restrict__ gather, T* __restrict__ R2, T* __restrict__ P2f, LevelArgs<T> a,
+                int* flag) {
+  constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int e1 = int(a.e[1]), e2 = int(a.e[2]);
+  const int c1 = int(a.c[1]), c2 = int(a.c[2]);
+  const int j = blockIdx.x;
+  const int64_t plane = int64_t(e1) * e2;
+  const T* Up = U + j * plane;
+  auto coarse = [&](int64_t b0, int64_t b1, int64_t b2) {
+    return U[(2 * b0) * plane + (2 * b1) * e2 + 2 * b2];
+  };
+  bool bad = false;
+  const int i0 = int(blockIdx.z) * kFaceItems;
+  if (blockIdx.y == 0) {
+    const T t0 = a.taps[2][int64_t(c2 - 1) * 5 + 0], t1 = a.taps[2][int64_t(c2 - 1) * 5 + 1],
+            t2 = a.taps[2][int64_t(c2 - 1) * 5 + 2];
+    const int i1 = min(e1, i0 + kFaceItems);
+    for (int r = i0 + int(threadIdx.x); r < i1; r += blockDim.x) {
+      const T* row = Up + int64_t(r) * e2 + (e2 - 3);
+      const T u0 = row[0], u1 = row[1], u2 = row[2];
+      const bool masked = REC && !((j | r) & 1);  // e2-3 and e2-1 are even columns
+      R2[int64_t(j) * e1 + r] = masked ? t1 * u1 : t0 * u0 + t1 * u1 + t2 * u2;
+      if (masked)  // a coarse node of the last coarse column
+        gather[((int64_t(j) >> 1) * c1 + (r >> 1)) * c2 + (c2 - 1)] = u2;
+      if (DEC) {
+        bad |= !isfinite(u2);
+        if ((j | r) & 1)  // never a side cell: the column is even
+          coef_out[j * plane + int64_t(r) * e2 + (e2 - 1)] = u2 - interp_node(a, j, r, e2 - 1, coarse);
+      }
+    }
+  } else {
+    // P2f: 3 rows x (c2 - 1) coarse columns
+    const int n = 3 * (c2 - 1);
+    const int i1 = min(n, i0 + kFaceItems);
+    for (int it = i0 + int(threadIdx.x); it < i1; it += blockDim.x) {
+      const int y = it / (c2 - 1), q2 = it - y * (c2 - 1);
+      const int r = e1 - 3 + y;
+      const T* row = Up + int64_t(r) * e2;
+      const bool maskrow = REC && !((j | r) & 1);
+      T acc = T(0);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int f = 2 * q2 - 2 + k;
+        if (f < 0 || f >= e2) continue;
+        const bool masked = maskrow && !(f & 1);
+        acc += a.taps[2][int64_t(q2) * 5 + k] * (masked ? T(0) : row[f]);
+      }
+      P2f[(int64_t(j) * 3 + y) * c2 + q2] = acc;
+      if (REC && y == 2 && !(j & 1))  // a coarse node of the last coarse row
+        gather[((int64_t(j) >> 1) * c1 + (c1 - 1)) * c2 + q2] = row[2 * q2];
+    }
+    if (DEC) {  // the last fine row, columns < e2-1 (contiguous)
+      const int r = e1 - 1;
+      const int ic1 = min(e2 - 1, i0 + kFaceItems);
+      for (int c = i0 + int(threadIdx.x); c < ic1; c += blockDim.x) {
+        const int64_t idx = j * plane + int64_t(r) * e2 + c;
+        const T u = U[idx];
+        bad |= !isfinite(u);
+        if ((j | c) & 1) {  // r = e1-1 is even
+          const T cv = u - interp_node(a, j, r, c, coarse);
+          if (side != nullptr && !(j & 1))  // even row of an even plane (c odd)
+            side[((j >> 1) * int64_t(c1) + (r >> 1)) * (c2 - 1) + (c >> 1)] = cv;
+          else
+            coef_out[idx] = cv;
+        }
+      }
+    }
+  }
+  if (DEC && flag && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <class T, int MODE>
+__global__ void __launch_bounds__(256)
+    k_face_zload(T* __restrict__ zload, const T* __restrict__ R2, const T* __restrict__ P2f,
+                 LevelArgs<T> a) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int e0 = int(a.e[0]), e1 = int(a.e[1]), e2 = int(a.e[2]);
+  const int c0 = int(a.c[0]), c1 = int(a.c[1]), c2 = int(a.c[2]);
+  const int i0 = blockIdx.x;
+  if (i0 >= c0) return;
+  T w0[5];
+  int f0[5];
+#pragma unroll
+  for (int x = 0; x < 5; ++x) {
+    f0[x] = 2 * i0 - 2 + x;
+    w0[x] = (f0[x] < 0 || f0[x] >= e0) ? T(0) : e0 == 1 ? T(1) : a.taps[0][int64_t(i0) * 5 + x];
+    if (f0[x] < 0 || f0[x] >= e0) f0[x] = 0;
+  }
+  const int q = int(blockIdx.z) * blockDim.x + threadIdx.x;
+  if (blockIdx.y == 0) {  // last coarse column, every coarse row
+    if (q >= c1) return;
+    T acc = T(0);
+#pragma unroll
+    for (int x = 0; x < 5; ++x) {
+      const T* R = R2 + int64_t(f0[x]) * e1;
+      T s = T(0);
+#pragma unroll
+      for (int y = 0; y < 5; ++y) {
+        const int f = 2 * q - 2 + y;
+        if (f >= 0 && f < e1) s += a.taps[1][int64_t(q) * 5 + y] * R[f];
+      }
+      acc += w0[x] * s;
+    }
+    const int64_t o = (int64_t(i0) * c1 + q) * c2 + (c2 - 1);
+    zload[o] = acc;
+  } else {  // last coarse row, columns < c2-1
+    if (q >= c2 - 1) return;
+    T k1[3];
+#pragma unroll
+    for (int y = 0; y < 3; ++y) k1[y] = a.taps[1][int64_t(c1 - 1) * 5 + y];
+    T acc = T(0);
+#pragma unroll
+    for (int x = 0; x < 5; ++x) {
+      const T* Pp = P2f + int64_t(f0[x]) * 3 * c2 + q;
+      acc += w0[x] * (k1[0] * Pp[0] + k1[1] * Pp[c2] + k1[2] * Pp[2 * c2]);
+    }
+    const int64_t o = (int64_t(i0) * c1 + (c1 - 1)) * c2 + q;
+    zload[o] = acc;
+  }
+}
+
 template <class T, int MODE>
 void set_level_face_smem(size_t bytes) {
   if (bytes > 48 * 1024) set_smem_attr(reinterpret_cast<const void*>(k_level_face<T, MODE>), bytes);
@@ -768,7 +908,7 @@ int fused_heuristic_s0(const LevelArgs<T>& a) {
 
 template <class T, int MODE>
 void run_fused(const T* U, T* coef, T* z, T* gather, T* side, const LevelArgs<T>& a, int* flag,
-               cudaStream_t s, int s0) {
+               cudaStream_t s, int s0, T* face_ws) {
   using C = LCfg<T>;
   auto kern = k_level_fused<T, MODE>;
   set_smem_attr(reinterpret_cast<const void*>(kern), C::total);
@@ -799,6 +939,20 @@ void run_fused(const T* U, T* coef, T* z, T* gather, T* side, const LevelArgs<T>
                gather, side, a, S0, nt1, nt2, nseg, sa, flag);
     sa = sb;
   }
+  // two-phase faces for levels with large faces (one launch each below: the
+  // small levels are launch-latency bound)
+  if (face_ws != nullptr && a.e[0] * a.e[1] >= (int64_t(1) << 18)) {
+    T* R2 = face_ws;
+    T* P2f = face_ws + a.e[0] * a.e[1];
+    const int64_t n1 = std::max({a.e[1], 3 * (a.c[2] - 1), a.e[2] - 1});
+    launch_pdl(k_face_slab<T, MODE>,
+               dim3(unsigned(a.e[0]), 2, unsigned((n1 + kFaceItems - 1) / kFaceItems)), dim3(256), 0, s,
+               a.e[0] * a.e[1] * a.e[2], U, coef, side, gather, R2, P2f, a, flag);
+    const int64_t n2 = std::max(a.c[1], a.c[2]);
+    launch_pdl(k_face_zload<T, MODE>, dim3(unsigned(a.c[0]), 2, unsigned((n2 + 255) / 256)), dim3(256),
+               0, s, a.e[0] * a.e[1] * a.e[2], z, R2, P2f, a);
+    return;
+  }
   const int64_t fseg =
       std::max((std::max(a.c[1], a.c[2]) + kFaceSeg - 1) / kFaceSeg,
                MODE == kFusedDecompose ? (std::max(a.e[1], a.e[2]) + kFaceCells - 1) / kFaceCells : 0);
@@ -814,7 +968,7 @@ void run_fused(const T* U, T* coef, T* z, T* gather, T* side, const LevelArgs<T>
 
 template <class T>
 bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const LevelArgs<T>& a,
-                        int mode, int* flag, cudaStream_t s, int s0, T* side) {
+                        int mode, int* flag, cudaStream_t s, int s0, T* side, T* face_ws) {
   // TMA needs a 16-byte aligned base; dim 0 segments need c0-1 = 2^k
   if (a.e[0] == 1 && a.e[1] == 1) {
     require(side == nullptr, "side rows are a 2D / 3D decompose option");
@@ -825,11 +979,11 @@ bool launch_level_fused(const T* U, T* coef_out, T* zload, T* gather, const Leve
   if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
   require(side == nullptr || mode == kFusedDecompose, "side rows are a decompose option");
   if (mode == kFusedDecompose)
-    run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, side, a, flag, s, s0);
+    run_fused<T, kFusedDecompose>(U, coef_out, zload, gather, side, a, flag, s, s0, face_ws);
   else if (mode == kFusedLoadOnly)
-    run_fused<T, kFusedLoadOnly>(U, coef_out, zload, gather, nullptr, a, flag, s, s0);
+    run_fused<T, kFusedLoadOnly>(U, coef_out, zload, gather, nullptr, a, flag, s, s0, face_ws);
   else
-    run_fused<T, kFusedRecompose>(U, coef_out, zload, gather, nullptr, a, flag, s, s0);
+    run_fused<T, kFusedRecompose>(U, coef_out, zload, gather, nullptr, a, flag, s, s0, face_ws);
   return true;
 }
 
@@ -873,9 +1027,10 @@ template std::vector<SegChoice> level_fused_candidates<double>(const LevelArgs<d
                                                                 double);
 
 template bool launch_level_fused<float>(const float*, float*, float*, float*,
-                                        const LevelArgs<float>&, int, int*, cudaStream_t, int, float*);
+                                        const LevelArgs<float>&, int, int*, cudaStream_t, int, float*,
+                                        float*);
 template bool launch_level_fused<double>(const double*, double*, double*, double*,
                                          const LevelArgs<double>&, int, int*, cudaStream_t, int,
-                                         double*);
+                                         double*, double*);
 
 }  // namespace hgrb

@@ -301,6 +301,9 @@ class PlanT final : public Plan {
   // even rows of even planes, merged into the output with the coarser pyramid by
   // k_merge_even (knob HGR_SIDE_ROWS=0: strided scatter instead)
   T* E_ = nullptr;
+  // face scratch of the fused level kernels (two-phase faces, kernels_level.cu);
+  // knob HGR_FACE2=0: the one-kernel faces instead
+  T* F_ = nullptr;
   bool side_used_ = false;
   // coarse tail: levels 1..tail_lt_ (all below the fused threshold, under the
   // top) run as one single-CTA launch per direction (kernels_tail.cu)
@@ -471,6 +474,17 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   }
   const std::size_t off_e = total;
   total += (e_n * esz + 511) & ~std::size_t(255);
+  std::size_t f_n = 0;
+  {
+    bool face2 = true;
+    if (const char* v = std::getenv("HGR_FACE2")) face2 = v[0] != '0';
+    for (int l = 1; l <= Lv && face2; ++l)
+      if (big(l))
+        f_n = std::max(f_n, std::size_t(level_face_ws_elems<T>(ext_[std::size_t(l)].data(),
+                                                                ext_[std::size_t(l) - 1].data())));
+  }
+  const std::size_t off_f = total;
+  total += (f_n * esz + 511) & ~std::size_t(255);
   const std::size_t off_s0 = total;
   total += (stage_n[0] * esz + 511) & ~std::size_t(255);
   const std::size_t off_s1 = total;
@@ -488,6 +502,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   for (int l = 1; l <= Lv; ++l) Z_[std::size_t(l)] = reinterpret_cast<T*>(ws_ + off_z[std::size_t(l)]);
   if (w_n) W_ = reinterpret_cast<T*>(ws_ + off_w);
   if (e_n) E_ = reinterpret_cast<T*>(ws_ + off_e);
+  if (f_n) F_ = reinterpret_cast<T*>(ws_ + off_f);
   stage_[0] = reinterpret_cast<T*>(ws_ + off_s0);
   {
     // one CTA is the better engine only while a level is a few thousand nodes
@@ -677,7 +692,8 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
       prof_begin(kKindFusedDec, sz() * (n + (n - c) + c), s);
       T* side = top ? E_ : nullptr;
       const bool ok = launch_level_fused<T>(src, coef_dst, z, nullptr, a, kFusedDecompose,
-                                            top ? d_flag_ : nullptr, s, s0_dec_[std::size_t(l)], side);
+                                            top ? d_flag_ : nullptr, s, s0_dec_[std::size_t(l)], side,
+                                            F_);
       prof_end(s);
       if (top) side_used_ = ok && side != nullptr;
       if (ok) {
@@ -688,7 +704,7 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
     } else {
       prof_begin(kKindFusedDec, sz() * (n + c), s);
       const bool ok = launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s,
-                                            s0_dec_[std::size_t(l)]);
+                                            s0_dec_[std::size_t(l)], nullptr, F_);
       prof_end(s);
       if (ok) {
         prof_begin(kKindSmall, sz() * (n + (n - c)), s);
@@ -844,7 +860,8 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
       T* zl = thomas_src(l, Z_[std::size_t(l)]);
       prof_begin(kKindFusedRec, sz() * (n + 2 * c), s);
       const bool ok = launch_level_fused<T>(src, nullptr, zl, C_[std::size_t(l) - 1], a,
-                                            kFusedRecompose, nullptr, s, s0_rec_[std::size_t(l)]);
+                                            kFusedRecompose, nullptr, s, s0_rec_[std::size_t(l)],
+                                            nullptr, F_);
       prof_end(s);
       if (ok) {
         ++launch_count_;
@@ -995,14 +1012,19 @@ std::string PlanT<T>::autotune(const void* d_in, void* d_out, cudaStream_t s) {
     T* z = Z_[std::size_t(l)];
     T* gat = C_[std::size_t(l) - 1];
     // operands the fused kernels accept (16-byte aligned); else the level is not fused
-    if (!launch_level_fused<T>(src, coef, z, nullptr, a, kFusedDecompose, nullptr, s)) continue;
+    if (!launch_level_fused<T>(src, coef, z, nullptr, a, kFusedDecompose, nullptr, s, 0, nullptr, F_))
+      continue;
     tune(l, "decompose_level", level_fused_candidates<T>(a, kFusedDecompose, bw),
          level_fused_default_s0<T>(a),
-         [&](int v) { launch_level_fused<T>(src, coef, z, nullptr, a, kFusedDecompose, nullptr, s, v); },
+         [&](int v) {
+           launch_level_fused<T>(src, coef, z, nullptr, a, kFusedDecompose, nullptr, s, v, nullptr, F_);
+         },
          s0_dec_[std::size_t(l)]);
     tune(l, "recompose_level", level_fused_candidates<T>(a, kFusedRecompose, bw),
          level_fused_default_s0<T>(a),
-         [&](int v) { launch_level_fused<T>(src, nullptr, z, gat, a, kFusedRecompose, nullptr, s, v); },
+         [&](int v) {
+           launch_level_fused<T>(src, nullptr, z, gat, a, kFusedRecompose, nullptr, s, v, nullptr, F_);
+         },
          s0_rec_[std::size_t(l)]);
     T* dst = l == Lv ? out : C_[std::size_t(l)];
     const T* cf = l == Lv ? in : C_[std::size_t(l)];
