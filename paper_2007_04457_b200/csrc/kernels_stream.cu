@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
   if (tid == 0) {
     for (int b = 0; b < nslot; ++b) {
       ptx::mbar_init(&full[b], 1);
-      ptx::mbar_init(&empty[b], NWC);
+      ptx::mbar_init(&empty[b], NWC * 32);  // every consumer lane arrives
     }
     ptx::fence_mbar_init();
   }
@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(NT + 32, 1)
       const T* col = S + ph0 + tid;
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = (act && r < B) ? col[r * G.SP] : T(0);
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[sl]);
+      ptx::mbar_arrive(&empty[sl]);  // each lane releases its own reads
       if (act) {
         T t1[R], t2[R];
         load_tab<T, R>(tm + s, t1);
@@ -444,14 +443,11 @@ __global__ void __launch_bounds__(NT + 32, 1)
     // writes of this warp ordered before the next bulk copy into them)
     if (nfin > 0) {
       ptx::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        for (int d = nfin - 1; d >= 0; --d) {
-          const int dd = last ? d : K;
-          int sf = sl - dd;
-          if (sf < 0) sf += nslot;
-          ptx::mbar_arrive(&empty[sf]);
-        }
+      for (int d = nfin - 1; d >= 0; --d) {  // each lane releases its own accesses
+        const int dd = last ? d : K;
+        int sf = sl - dd;
+        if (sf < 0) sf += nslot;
+        ptx::mbar_arrive(&empty[sf]);
       }
     }
     }  // !REGH
@@ -524,8 +520,8 @@ __global__ void __maxnreg__(ws_maxnreg((CW + RWN + 1) * 32))
   if (tid == 0) {
     for (int b = 0; b < nslot; ++b) {
       ptx::mbar_init(&full[b], 1);
-      ptx::mbar_init(&rowsd[b], RWN);
-      ptx::mbar_init(&empty[b], CW);
+      ptx::mbar_init(&rowsd[b], RWN * 32);  // every lane of the row warps arrives
+      ptx::mbar_init(&empty[b], CW * 32);  // every lane of the column warps arrives
     }
     ptx::fence_mbar_init();
   }
@@ -643,8 +639,7 @@ __global__ void __maxnreg__(ws_maxnreg((CW + RWN + 1) * 32))
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&rowsd[sl]);
+      ptx::mbar_arrive(&rowsd[sl]);  // each lane releases its own row writes
       if (++sl == nslot) {
         sl = 0;
         ++use;
@@ -685,8 +680,7 @@ __global__ void __maxnreg__(ws_maxnreg((CW + RWN + 1) * 32))
 #pragma unroll
       for (int r = 0; r < R; ++r) x[u][r] = (c < P && r < B) ? S[r * P + c] : T(0);
     }
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[sl]);
+    ptx::mbar_arrive(&empty[sl]);  // each lane releases its own reads
     if (b == 0) {
 #pragma unroll
       for (int u = 0; u < CPT; ++u) yprev[u] = T(0);
