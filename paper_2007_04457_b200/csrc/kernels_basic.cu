@@ -358,35 +358,44 @@ __global__ void __launch_bounds__(1024) k_merge_even(const T* __restrict__ coars
       const T* base = ring + (int64_t(st) * R + r) * 2 * RE;
       const T* cr = base + int((rr * c2) & (V - 1));
       const T* sr = base + RE + int((rr * (c2 - 1)) & (V - 1));
-      const int64_t q0 = rr / c1, q1 = rr - q0 * c1;
-      const int64_t g = ((2 * q0) * e1 + 2 * q1) * e2;
+      const int q0 = int(rr) / int(c1), q1 = int(rr) - q0 * int(c1);  // rows < 2^31
+      const int64_t g = ((2 * int64_t(q0)) * e1 + 2 * q1) * e2;
       const int ph = int(g & (V - 1));
       const int nvec = int((ph + e2 + V - 1) / V);
       T* orow = out + (g - ph);
-      for (int u = tid; u < nvec; u += blockDim.x) {
-        T v[V];
-        bool full = true;
+      VT* ov = reinterpret_cast<VT*>(orow);
+      // output position p = u*V + k - ph: even p from the coarse row, odd from the
+      // side row. Interior vectors are whole: no range checks, parity fixed by ph.
+      auto edge = [&](int u) {
 #pragma unroll
         for (int k = 0; k < V; ++k) {
           const int p = u * V + k - ph;
-          const bool in = p >= 0 && p < e2;
-          full = full && in;
-          v[k] = !in ? T(0) : (p & 1) ? sr[p >> 1] : cr[p >> 1];
+          if (p >= 0 && p < e2) orow[u * V + k] = (p & 1) ? sr[p >> 1] : cr[p >> 1];
         }
-        if (full) {
+      };
+      if (tid == 0) edge(0);
+      if (tid == 1 && nvec > 1) edge(nvec - 1);
+      if (!(ph & 1)) {
+        for (int u = 1 + tid; u < nvec - 1; u += blockDim.x) {
+          const int a = (u * V - ph) >> 1;
           VT w;
           if constexpr (V == 4) {
-            w.x = v[0]; w.y = v[1]; w.z = v[2]; w.w = v[3];
+            w.x = cr[a]; w.y = sr[a]; w.z = cr[a + 1]; w.w = sr[a + 1];
           } else {
-            w.x = v[0]; w.y = v[1];
+            w.x = cr[a]; w.y = sr[a];
           }
-          reinterpret_cast<VT*>(orow)[u] = w;
-        } else {
-#pragma unroll
-          for (int k = 0; k < V; ++k) {
-            const int p = u * V + k - ph;
-            if (p >= 0 && p < e2) orow[u * V + k] = v[k];
+          ov[u] = w;
+        }
+      } else {
+        for (int u = 1 + tid; u < nvec - 1; u += blockDim.x) {
+          const int a = (u * V - ph) >> 1;
+          VT w;
+          if constexpr (V == 4) {
+            w.x = sr[a]; w.y = cr[a + 1]; w.z = sr[a + 1]; w.w = cr[a + 2];
+          } else {
+            w.x = sr[a]; w.y = cr[a + 1];
           }
+          ov[u] = w;
         }
       }
     }
