@@ -103,6 +103,12 @@ void launch_merge_even(const T* coarse, const T* side, T* out, const LevelArgs<T
 // Recompose interpolation (GPK^-1, refactor.hpp:77-87): coarse = C - Z (Z may be
 // null), out[coarse] = coarse, out[refined] = (with ? coef : 0) + interp(coarse).
 // 3D tiles with the coarse block staged in shared memory. in-place safe.
+// In-place coefficients of a fused level (the in-place decompose): U becomes
+// U - interp(C) at refined nodes, C = the gathered coarse nodes; the
+// interpolation march in subtract mode; flag: non-finite input seen.
+template <class T>
+bool launch_coef_inplace(T* U, const T* C, const LevelArgs<T>& a, int* flag, cudaStream_t s,
+                         int s0 = 0);
 template <class T>
 bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const LevelArgs<T>& a,
                        bool with_coeffs, cudaStream_t s, int s0 = 0);

@@ -138,12 +138,15 @@ __device__ __forceinline__ void ldnc(const T* row, int pos, T (&v)[N]) {
   }
 }
 
-template <class T, bool WITH, bool HASZ>
+// SUB (in-place decompose): out = U - interp(C) at refined nodes, U at coarse
+// nodes, with U in place of the coefficients (every cell reads only its own U,
+// the coarse values come from C) and a non-finite check of every cell into flag.
+template <class T, bool WITH, bool HASZ, bool SUB>
 __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     k_interp_march(const __grid_constant__ CUtensorMap mcoef, const __grid_constant__ CUtensorMap mC,
                    const __grid_constant__ CUtensorMap mZ, int64_t coef_off, int64_t c_off,
                    T* __restrict__ out, LevelArgs<T> a, int S0, int nt1, int nt2, int nseg,
-                   int seg_base) {
+                   int seg_base, int* flag) {
   using C = ICfg<T>;
   ptx::pdl_trigger();
   constexpr int V = C::V, PITCH = C::PITCH, SLOT = C::SLOT, NS = C::NS, NW = C::NW;
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
 #pragma unroll
     for (int k = 0; k < NC1; ++k) A1p[i][k] = A1[i][k] = T(0);
   T* obase = out + (2 * q1a + b) * e2 + 2 * q2a + 2 * t0;
+  T bad = T(0);  // SUB: non-finite input seen
 
   // one fine plane j: out = coef + interp (interp alone at coarse nodes / without coef)
   auto fine_plane = [&](int64_t j, bool odd, T w0l, T w0r) {
@@ -312,9 +316,18 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
           cf[NCELL] = fk == NCELL ? rowp[pos + NCELL] : T(0);
         }
 #pragma unroll
-        for (int k = 0; k < NC1; ++k)
+        for (int k = 0; k < NC1; ++k) {
           // the coarse nodes (even plane, even row, even column) keep the interpolant
-          if (odd || (i & 1) || (k & 1)) v[k] += cf[k];
+          // (SUB: keep U there, the coefficient U - interp elsewhere)
+          const bool refined = odd || (i & 1) || (k & 1);
+          if constexpr (SUB) {
+            v[k] = refined ? cf[k] - v[k] : cf[k];
+            if (rown[i] && (k < NCELL ? cvalid[k >> 1] || k == fk : fk == NCELL))
+              bad = cf[k] * T(0) + bad;
+          } else if (refined) {
+            v[k] += cf[k];
+          }
+        }
       }
       if (rown[i]) {
         T* orow = o + int64_t(i) * e2;
@@ -413,6 +426,10 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     }
     if (m + 2 <= kb) issue_c(m + 2);
   }
+  if (SUB && flag) {
+    const bool nf = !(bad == T(0));
+    if (__syncthreads_or(nf) && tid == 0) atomicOr(flag, 1);
+  }
 }
 
 // The last fine column (e2-1, blockIdx.y = 0) and row (e1-1, columns < e2-1,
@@ -462,11 +479,11 @@ int interp_heuristic_s0(const LevelArgs<T>& a) {
   return S0;
 }
 
-template <class T, bool WITH, bool HASZ>
+template <class T, bool WITH, bool HASZ, bool SUB = false>
 void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs<T>& a,
-                cudaStream_t s, int s0) {
+                cudaStream_t s, int s0, int* flag = nullptr) {
   using Cf = ICfg<T>;
-  auto kern = k_interp_march<T, WITH, HASZ>;
+  auto kern = k_interp_march<T, WITH, HASZ, SUB>;
   set_smem_attr(reinterpret_cast<const void*>(kern), Cf::total);
   const int nt1 = int((a.c[1] - 1 + Cf::TW1 - 1) / Cf::TW1);
   const int nt2 = int((a.c[2] - 1 + Cf::TW2 - 1) / Cf::TW2);
@@ -495,7 +512,7 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
     if (WITH) make_tma_1d(&mcoef, coef + coef_off, uint64_t(Nf - coef_off), int(sizeof(T)), Cf::BOX);
     const int64_t blocks = tiles * (sb - sa);
     launch_pdl(kern, dim3(unsigned(blocks)), dim3(Cf::NT), Cf::total, s, Nf, mcoef, mC, mZ, coef_off, c_off, out, a, S0,
-                                                     nt1, nt2, nseg, sa);
+                                                     nt1, nt2, nseg, sa, flag);
     HGR_CUDA_CHECK(cudaGetLastError());
     sa = sb;
   }
@@ -516,6 +533,18 @@ bool launch_interp_rec(const T* coef, T* out, const T* C, const T* Z, const Leve
   else if (Z) run_interp<T, false, true>(coef, out, C, Z, a, s, s0);
   else run_interp<T, false, false>(coef, out, C, Z, a, s, s0);
   // the faces (last fine row / column) are written by the last tiles
+  return true;
+}
+
+template <class T>
+bool launch_coef_inplace(T* U, const T* C, const LevelArgs<T>& a, int* flag, cudaStream_t s,
+                         int s0) {
+  if (a.e[0] == 1 && a.e[1] == 1) return false;  // 1D: the line kernels
+  const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (a.e[1] < 3 || a.e[2] < 3 || !al(C) || !al(U)) return false;
+  if (a.c[0] > 1 && ((a.c[0] - 1) & (a.c[0] - 2)) != 0) return false;
+  if (a.c[0] * a.c[1] * a.c[2] >= (int64_t(1) << 31)) return false;
+  run_interp<T, true, false, true>(U, U, C, nullptr, a, s, s0, flag);
   return true;
 }
 
@@ -563,5 +592,9 @@ template bool launch_interp_rec<float>(const float*, float*, const float*, const
                                        const LevelArgs<float>&, bool, cudaStream_t, int);
 template bool launch_interp_rec<double>(const double*, double*, const double*, const double*,
                                         const LevelArgs<double>&, bool, cudaStream_t, int);
+template bool launch_coef_inplace<float>(float*, const float*, const LevelArgs<float>&, int*,
+                                         cudaStream_t, int);
+template bool launch_coef_inplace<double>(double*, const double*, const LevelArgs<double>&, int*,
+                                          cudaStream_t, int);
 
 }  // namespace hgrb

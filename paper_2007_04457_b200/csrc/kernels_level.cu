@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
           else loadV<T, NV>(S + r * PITCH, rph(phj, r), wb, v);
           const bool masked = !jodd && !(r & 1);
           k2row(v, masked, P2 + r * P2W);
-          if (REC && masked && i < 4 && rown[i] && j >= 2 * ka && j < 2 * kb) {
+          if ((REC || (MODE == kFusedLoadOnly && gather != nullptr)) && masked && i < 4 &&
+              rown[i] && j >= 2 * ka && j < 2 * kb) {
             // gather the coarse nodes of this row into C_{l-1}
             T* gd = gather + ((j >> 1) * c1 + ((wr0 + r) >> 1)) * c2 + q2a + t0;
 #pragma unroll
@@ -714,7 +715,8 @@ __global__ void __launch_bounds__(256)
       const int i1 = face == 0 ? q : c1 - 1, i2 = face == 0 ? c2 - 1 : q;
       const int64_t o = (int64_t(i0) * c1 + i1) * c2 + i2;
       zload[o] = acc;
-      if (REC) gather[o] = U[(2 * int64_t(i0)) * plane + int64_t(2 * i1) * e2 + 2 * i2];
+      if (REC || (MODE == kFusedLoadOnly && gather != nullptr))
+        gather[o] = U[(2 * int64_t(i0)) * plane + int64_t(2 * i1) * e2 + 2 * i2];
     }
     return;
   }
@@ -764,6 +766,7 @@ __global__ void __launch_bounds__(256)
                 T* __restrict__ gather, T* __restrict__ R2, T* __restrict__ P2f, LevelArgs<T> a,
                 int* flag) {
   constexpr bool DEC = MODE == kFusedDecompose, REC = MODE == kFusedRecompose;
+  constexpr bool GATHER = MODE != kFusedDecompose;  // recompose; load-only when asked
   ptx::pdl_trigger();
   ptx::pdl_wait();
   const int e1 = int(a.e[1]), e2 = int(a.e[2]);
@@ -785,7 +788,7 @@ __global__ void __launch_bounds__(256)
       const T u0 = row[0], u1 = row[1], u2 = row[2];
       const bool masked = REC && !((j | r) & 1);  // e2-3 and e2-1 are even columns
       R2[int64_t(j) * e1 + r] = masked ? t1 * u1 : t0 * u0 + t1 * u1 + t2 * u2;
-      if (masked)  // a coarse node of the last coarse column
+      if (GATHER && gather != nullptr && !((j | r) & 1))  // a coarse node of the last coarse column
         gather[((int64_t(j) >> 1) * c1 + (r >> 1)) * c2 + (c2 - 1)] = u2;
       if (DEC) {
         bad |= !isfinite(u2);
@@ -811,7 +814,7 @@ __global__ void __launch_bounds__(256)
         acc += a.taps[2][int64_t(q2) * 5 + k] * (masked ? T(0) : row[f]);
       }
       P2f[(int64_t(j) * 3 + y) * c2 + q2] = acc;
-      if (REC && y == 2 && !(j & 1))  // a coarse node of the last coarse row
+      if (GATHER && gather != nullptr && y == 2 && !(j & 1))  // a coarse node of the last coarse row
         gather[((int64_t(j) >> 1) * c1 + (c1 - 1)) * c2 + q2] = row[2 * q2];
     }
     if (DEC) {  // the last fine row, columns < e2-1 (contiguous)

@@ -240,6 +240,7 @@ class PlanT final : public Plan {
 
   void decompose_to(const void* d_in, void* d_out, cudaStream_t s) override;
   void decompose_to_direct(const void* d_in, void* d_out, cudaStream_t s);
+  void decompose_direct(void* d_data, cudaStream_t s);
   void recompose_direct(const void* d_in, void* d_out, int upto, cudaStream_t s);
 
  private:
@@ -702,13 +703,17 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
         return;
       }
     } else {
-      prof_begin(kKindFusedDec, sz() * (n + c), s);
-      const bool ok = launch_level_fused<T>(src, nullptr, z, nullptr, a, kFusedLoadOnly, nullptr, s,
+      // in place: the load vector and the coarse gather in one read of the level,
+      // then the coefficients in place by the interpolation march in subtract mode
+      prof_begin(kKindFusedDec, sz() * (n + 2 * c), s);
+      const bool ok = launch_level_fused<T>(src, nullptr, z, Cn, a, kFusedLoadOnly, nullptr, s,
                                             s0_dec_[std::size_t(l)], nullptr, F_);
       prof_end(s);
       if (ok) {
-        prof_begin(kKindSmall, sz() * (n + (n - c)), s);
-        launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);  // coefficients in place
+        prof_begin(kKindInterp, sz() * (n + (n - c) + c), s);
+        const bool sub = launch_coef_inplace<T>(coef_dst, Cn, a, top ? d_flag_ : nullptr, s,
+                                                s0_int_[std::size_t(l)]);
+        if (!sub) launch_gpk_dec<T>(coef_dst, Cn, a, d_flag_, top, s);  // coefficients in place
         prof_end(s);
         launch_count_ += 2;
         thomas_all(l, z, Cn, s);
@@ -800,6 +805,11 @@ void PlanT<T>::decompose_to_direct(const void* d_in, void* d_out, cudaStream_t s
 
 template <class T>
 void PlanT<T>::decompose(void* d_data, cudaStream_t s) {
+  run_graphed(2, d_data, d_data, 0, s, [&](cudaStream_t st) { decompose_direct(d_data, st); });
+}
+
+template <class T>
+void PlanT<T>::decompose_direct(void* d_data, cudaStream_t s) {
   T* data = static_cast<T*>(d_data);
   launch_count_ = 0;
   HGR_CUDA_CHECK(cudaMemsetAsync(d_flag_, 0, sizeof(int), s));
