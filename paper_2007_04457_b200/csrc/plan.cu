@@ -3,11 +3,14 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
@@ -15,6 +18,31 @@
 #include "tables.hpp"
 
 namespace hgrb {
+
+namespace {
+// NVTX ranges per level and phase for nsys / ncu timelines (knob HGR_NVTX=1;
+// header-only NVTX v3: no cost unless a tool is attached and the knob is set)
+bool nvtx_on() {
+  static const bool v = [] {
+    const char* e = std::getenv("HGR_NVTX");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+struct NvtxScope {
+  bool on;
+  NvtxScope(const char* what, int l) : on(nvtx_on()) {
+    if (!on) return;
+    char b[64];
+    std::snprintf(b, sizeof b, "%s %d", what, l);
+    nvtxRangePushA(b);
+  }
+  ~NvtxScope() {
+    if (on) nvtxRangePop();
+  }
+};
+}  // namespace
+
 
 // ---- Hierarchy (grid_hierarchy.hpp:51-188) ------------------------------------
 
@@ -682,6 +710,7 @@ void PlanT<T>::thomas_all(int l, T* src, T* last_out, cudaStream_t s) {
 // coef_dst and the corrected level-(l-1) nodal values into C_{l-1}.
 template <class T>
 void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, cudaStream_t s) {
+  NvtxScope nv("decompose level", l);
   const LevelArgs<T>& a = args_[std::size_t(l)];
   T* Cn = C_[std::size_t(l) - 1];
   T* z = Z_[std::size_t(l)];
@@ -744,6 +773,7 @@ void PlanT<T>::decompose_level(int l, const T* src, T* coef_dst, bool in_place, 
 // of level l (C_0 -> D_1 -> ... -> D_{L-1} -> out)
 template <class T>
 void PlanT<T>::assemble(T* out, cudaStream_t s) {
+  NvtxScope nv("assemble pyramid levels", L());
   const int Lv = L();
   for (int l = 1; l <= Lv; ++l) {
     const T* src = l == 1 ? C_[0] : D_[std::size_t(l) - 1];
@@ -862,6 +892,7 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     ++launch_count_;
   }
   for (int l = m; l > tail_lt_; --l) {
+    NvtxScope nv("recompose correction level", l);
     const T* src = l == Lv ? in : C_[std::size_t(l)];
     const LevelArgs<T>& a = args_[std::size_t(l)];
     const double n = double(h.node_count(l)), c = double(h.node_count(l - 1));
@@ -893,6 +924,7 @@ void PlanT<T>::recompose_direct(const void* d_in, void* d_out, int m, cudaStream
     ++launch_count_;
   }
   for (int l = tail_lt_ + 1; l <= Lv; ++l) {
+    NvtxScope nv("recompose interpolation level", l);
     const bool with = l <= m;
     const T* coef = l == Lv ? in : C_[std::size_t(l)];
     T* dst = l == Lv ? out : C_[std::size_t(l)];
