@@ -5,7 +5,8 @@ against the reference itself (oracle/_ref/libhgr_ref.so, the unmodified
 reference headers, run on this box's host cores).
 
 Compared at north_star's tolerance (max-abs / max|u| <= 1e-12 fp64, 1e-5 fp32):
-* the decompose pyramid against the reference's,
+* the decompose pyramid against the reference's (out of place and through the
+  in-place entry point),
 * the full recompose of the reference's pyramid against the reference's,
 * a prefix recompose (classes 0..L-2) against the reference's,
 * the GPU round trip against the input.
@@ -61,6 +62,13 @@ def _run(cuda, ref, parity_log, dt):
     plan.decompose_into(u, gpu_p)
     plan.sync_status()
     errs["decompose"] = _rel(gpu_p, ref_p_dev, scale)
+    # the in-place entry point (hgr_cuda_decompose_* / Plan.decompose_): its own
+    # schedule (load-only level kernel + in-place coefficients), same result
+    inplace = u.clone()
+    plan.decompose_(inplace)
+    plan.sync_status()
+    errs["decompose_in_place"] = _rel(inplace, ref_p_dev, scale)
+    del inplace
     back = torch.empty_like(u)
     plan.recompose_into(gpu_p, back, L)
     errs["round_trip"] = _rel(back, u, scale)
@@ -90,6 +98,7 @@ def test_1025_f64_vs_reference(cuda, ref, parity_log):
 
 def test_1025_f32_vs_reference(cuda, ref, parity_log):
     errs = _run(cuda, ref, parity_log, np.float32)
-    for k in ("decompose", "round_trip", "recompose_upto_10", "recompose_upto_8"):
+    for k in ("decompose", "decompose_in_place", "round_trip", "recompose_upto_10",
+              "recompose_upto_8"):
         assert errs[k] <= 1e-5, f"{k}: {errs[k]:.3e}"
     assert errs["gpu_f32_vs_ref_f64"] <= 10 * errs["ref_f32_vs_ref_f64"], errs
