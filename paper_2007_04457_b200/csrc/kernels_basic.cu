@@ -296,10 +296,15 @@ struct MergeCfg {
   static constexpr int V = 16 / int(sizeof(T));
   static __host__ __device__ int64_t row_elems(int64_t c2) { return (c2 + 2 * V - 1) / V * V; }  // superset + slack
   static size_t smem(int64_t c2) {
-    return size_t(kMergeStages) * kMergeRows * 2 * size_t(row_elems(c2)) * sizeof(T) + kMergeStages * 8;
+    return size_t(kMergeStages) * kMergeRows * 2 * size_t(row_elems(c2)) * sizeof(T) +
+           2 * kMergeStages * 8;
   }
 };
 
+// One producer warp (the last) streams groups of R coarse rows + side rows into a
+// ring of stages (full[st]: bytes landed); the consumer threads write the output
+// rows whole and hand a stage back (empty[st]: every consumer arrived) -- no CTA
+// barrier between groups.
 template <class T>
 __global__ void __launch_bounds__(1024) k_merge_even(const T* __restrict__ coarse,
                                                      const T* __restrict__ side, T* __restrict__ out,
@@ -310,47 +315,59 @@ __global__ void __launch_bounds__(1024) k_merge_even(const T* __restrict__ coars
   const int64_t c1 = a.c[1], c2 = a.c[2], e1 = a.e[1], e2 = a.e[2];
   const int64_t rows = a.c[0] * c1, RE = MergeCfg<T>::row_elems(c2);
   extern __shared__ __align__(16) unsigned char smem_m[];
-  constexpr int R = kMergeRows;
+  constexpr int R = kMergeRows, S = kMergeStages;
   T* ring = reinterpret_cast<T*>(smem_m);  // [stage][row][coarse row | side row]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ring + kMergeStages * R * 2 * RE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + S * R * 2 * RE);
+  uint64_t* empty = full + S;
   const int tid = threadIdx.x;
+  const int nc = int(blockDim.x) - 32;  // consumer threads
   if (tid == 0) {
-    for (int k = 0; k < kMergeStages; ++k) ptx::mbar_init(&bar[k], 1);
+    for (int k = 0; k < S; ++k) {
+      ptx::mbar_init(&full[k], 1);
+      ptx::mbar_init(&empty[k], nc);
+    }
     ptx::fence_mbar_init();
   }
   __syncthreads();
   const int64_t groups = (rows + R - 1) / R;  // a group = R consecutive rows
-  auto issue = [&](int64_t grp, int st) {     // tid 0
-    uint32_t total = 0;
-    for (int r = 0; r < R; ++r) {
-      const int64_t rr = grp * R + r;
-      if (rr >= rows) break;
-      const int64_t cb = rr * c2, sb = rr * (c2 - 1);
-      const int pc = int(cb & (V - 1)), ps = int(sb & (V - 1));
-      total += uint32_t((pc + c2 + V - 1) / V * V * sizeof(T)) +
-               uint32_t((ps + c2 - 1 + V - 1) / V * V * sizeof(T));
-    }
-    ptx::mbar_arrive_expect_tx(&bar[st], total);
-    for (int r = 0; r < R; ++r) {
-      const int64_t rr = grp * R + r;
-      if (rr >= rows) break;
-      const int64_t cb = rr * c2, sb = rr * (c2 - 1);
-      const int pc = int(cb & (V - 1)), ps = int(sb & (V - 1));
-      T* dst = ring + (int64_t(st) * R + r) * 2 * RE;
-      ptx::bulk_g2s(dst, coarse + (cb - pc), uint32_t((pc + c2 + V - 1) / V * V * sizeof(T)), &bar[st]);
-      ptx::bulk_g2s(dst + RE, side + (sb - ps), uint32_t((ps + c2 - 1 + V - 1) / V * V * sizeof(T)),
-                    &bar[st]);
-    }
-  };
   const int64_t G = gridDim.x;
   ptx::pdl_wait();
-  if (tid == 0)
-    for (int k = 0; k < kMergeStages; ++k)
-      if (blockIdx.x + k * G < groups) issue(blockIdx.x + k * G, k);
+  if (tid >= nc) {
+    // ---- producer warp (lane 0)
+    if (tid != nc) return;
+    int it = 0;
+    for (int64_t grp = blockIdx.x; grp < groups; grp += G, ++it) {
+      const int st = it % S;
+      if (it >= S) ptx::mbar_wait(&empty[st], uint32_t(((it / S) - 1) & 1));
+      uint32_t total = 0;
+      for (int r = 0; r < R; ++r) {
+        const int64_t rr = grp * R + r;
+        if (rr >= rows) break;
+        const int64_t cb = rr * c2, sb = rr * (c2 - 1);
+        const int pc = int(cb & (V - 1)), ps = int(sb & (V - 1));
+        total += uint32_t((pc + c2 + V - 1) / V * V * sizeof(T)) +
+                 uint32_t((ps + c2 - 1 + V - 1) / V * V * sizeof(T));
+      }
+      ptx::mbar_arrive_expect_tx(&full[st], total);
+      for (int r = 0; r < R; ++r) {
+        const int64_t rr = grp * R + r;
+        if (rr >= rows) break;
+        const int64_t cb = rr * c2, sb = rr * (c2 - 1);
+        const int pc = int(cb & (V - 1)), ps = int(sb & (V - 1));
+        T* dst = ring + (int64_t(st) * R + r) * 2 * RE;
+        ptx::bulk_g2s(dst, coarse + (cb - pc), uint32_t((pc + c2 + V - 1) / V * V * sizeof(T)),
+                      &full[st]);
+        ptx::bulk_g2s(dst + RE, side + (sb - ps), uint32_t((ps + c2 - 1 + V - 1) / V * V * sizeof(T)),
+                      &full[st]);
+      }
+    }
+    return;
+  }
+  // ---- consumers
   int it = 0;
   for (int64_t grp = blockIdx.x; grp < groups; grp += G, ++it) {
-    const int st = it % kMergeStages;
-    ptx::mbar_wait(&bar[st], uint32_t((it / kMergeStages) & 1));
+    const int st = it % S;
+    ptx::mbar_wait(&full[st], uint32_t((it / S) & 1));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int64_t rr = grp * R + r;
@@ -376,31 +393,30 @@ __global__ void __launch_bounds__(1024) k_merge_even(const T* __restrict__ coars
       if (tid == 0) edge(0);
       if (tid == 1 && nvec > 1) edge(nvec - 1);
       if (!(ph & 1)) {
-        for (int u = 1 + tid; u < nvec - 1; u += blockDim.x) {
-          const int a = (u * V - ph) >> 1;
+        for (int u = 1 + tid; u < nvec - 1; u += nc) {
+          const int a0 = (u * V - ph) >> 1;
           VT w;
           if constexpr (V == 4) {
-            w.x = cr[a]; w.y = sr[a]; w.z = cr[a + 1]; w.w = sr[a + 1];
+            w.x = cr[a0]; w.y = sr[a0]; w.z = cr[a0 + 1]; w.w = sr[a0 + 1];
           } else {
-            w.x = cr[a]; w.y = sr[a];
+            w.x = cr[a0]; w.y = sr[a0];
           }
           ov[u] = w;
         }
       } else {
-        for (int u = 1 + tid; u < nvec - 1; u += blockDim.x) {
-          const int a = (u * V - ph) >> 1;
+        for (int u = 1 + tid; u < nvec - 1; u += nc) {
+          const int a0 = (u * V - ph) >> 1;
           VT w;
           if constexpr (V == 4) {
-            w.x = sr[a]; w.y = cr[a + 1]; w.z = sr[a + 1]; w.w = cr[a + 2];
+            w.x = sr[a0]; w.y = cr[a0 + 1]; w.z = sr[a0 + 1]; w.w = cr[a0 + 2];
           } else {
-            w.x = sr[a]; w.y = cr[a + 1];
+            w.x = sr[a0]; w.y = cr[a0 + 1];
           }
           ov[u] = w;
         }
       }
     }
-    __syncthreads();  // every thread is done with this stage: refill it
-    if (tid == 0 && grp + kMergeStages * G < groups) issue(grp + kMergeStages * G, st);
+    ptx::mbar_arrive(&empty[st]);  // this thread is done with the stage
   }
 }
 
@@ -568,7 +584,8 @@ void launch_merge_even(const T* coarse, const T* side, T* out, const LevelArgs<T
                        cudaStream_t s) {
   constexpr int64_t V = MergeCfg<T>::V;
   const int64_t nvec = (a.e[2] + 2 * V - 2) / V;
-  const int threads = int(std::min<int64_t>(1024, (nvec + 31) / 32 * 32));
+  // consumer threads cover a row's vectors once, plus the producer warp
+  const int threads = int(std::min<int64_t>(992, (nvec + 31) / 32 * 32)) + 32;
   const size_t smem = MergeCfg<T>::smem(a.c[2]);
   require(merge_even_fits<T>(a.c[2]), "merge_even: rows too long for the shared-memory ring");
   set_smem_attr(reinterpret_cast<const void*>(k_merge_even<T>), smem);
