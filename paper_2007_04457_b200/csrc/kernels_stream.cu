@@ -109,7 +109,7 @@ __device__ __forceinline__ void load_tab(const T* t, T (&v)[R]) {
 // NT consumer threads (one column each; ROWS: also a warp per row) plus one
 // producer warp that refills the ring: full[s] completes when slot s's bytes
 // have landed, empty[s] when every consumer warp has finished the band in it.
-template <class T, int NT, bool ROWS, int CHR, bool REGH>
+template <class T, int NT, bool ROWS, int CHR, int KR>
 __global__ void __launch_bounds__(NT + 32, 1)
     k_thomas_stream(const T* in, T* out, StreamGeo G, const T* __restrict__ mult,
                     const T* __restrict__ rpiv, const T* __restrict__ upper,
@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(NT + 32, 1)
 
   // ---- consumers
   T yprev = T(0);
-  T hprev[REGH ? R : 1];   // REGH: backward-local values of band b - 1
+  constexpr bool REGH = KR > 0;  // the KR pending bands live in registers
+  T hprev[REGH ? KR : 1][REGH ? R : 1];  // backward-local values of bands b-1 (, b-2)
   T h0r[kStreamKMax + 1];  // h0r[k]: first backward-local value of band b - k
 #pragma unroll
   for (int k = 0; k <= kStreamKMax; ++k) h0r[k] = T(0);
@@ -340,9 +341,10 @@ __global__ void __launch_bounds__(NT + 32, 1)
     if (b == 0) yprev = T(0);
     const bool last = b == nb - 1;
     if constexpr (REGH) {
-      // ---- K = 1: the column values go to registers and the slot back to the
-      // producer at once; band b-1's backward-local values wait in registers
-      // (hprev) for the carry c_b = h0(b)
+      // ---- K = KR <= 2: the column values go to registers and the slot back to
+      // the producer at once; the pending bands' backward-local values wait in
+      // registers (hprev) for their carries: c_b(b-1) = h0(b) (K = 1), c_b(b-2) =
+      // h0(b-1) + Q0(b-1) h0(b) (K = 2; exact at the line end)
       const bool act = tid < jb.w;
       T x[R];
       const T* col = S + ph0 + tid;
@@ -367,13 +369,35 @@ __global__ void __launch_bounds__(NT + 32, 1)
           h = (x[r] - t1[r] * h) * t2[r];  // tp = 0 past the line: h stays 0 there
           x[r] = h;
         }
-        if (b > 0) {  // band b-1 is full
-          load_tab<T, R>(tQ + (s - R), t1);
-          T* o = out + jb.g0 + int64_t(s - R) * G.pitch + tid;
+        if constexpr (KR == 1) {
+          if (b > 0) {  // band b-1 is full
+            load_tab<T, R>(tQ + (s - R), t1);
+            T* o = out + jb.g0 + int64_t(s - R) * G.pitch + tid;
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            *o = hprev[r] + h * t1[r];
-            o += G.pitch;
+            for (int r = 0; r < R; ++r) {
+              *o = hprev[0][r] + h * t1[r];
+              o += G.pitch;
+            }
+          }
+        } else {
+          if (b >= 2) {  // band b-2 (full)
+            const T cb = hprev[0][0] + q0b[b - 1] * h;
+            load_tab<T, R>(tQ + (s - 2 * R), t1);
+            T* o = out + jb.g0 + int64_t(s - 2 * R) * G.pitch + tid;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              *o = hprev[1][r] + cb * t1[r];
+              o += G.pitch;
+            }
+          }
+          if (last && b >= 1) {  // band b-1 (full), exactly
+            load_tab<T, R>(tQ + (s - R), t1);
+            T* o = out + jb.g0 + int64_t(s - R) * G.pitch + tid;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              *o = hprev[0][r] + h * t1[r];
+              o += G.pitch;
+            }
           }
         }
         if (last) {  // the line ends here: zero carry
@@ -385,7 +409,10 @@ __global__ void __launch_bounds__(NT + 32, 1)
           }
         }
 #pragma unroll
-        for (int r = 0; r < R; ++r) hprev[r] = x[r];
+        for (int r = 0; r < R; ++r) {
+          if constexpr (KR == 2) hprev[1][r] = hprev[0][r];
+          hprev[0][r] = x[r];
+        }
       }
     } else {
     // ---- columns: forward with the exact carry, backward-local (kept in the
@@ -815,7 +842,7 @@ constexpr size_t kStreamSmem = 220 * 1024;
 // Fill the ring geometry for a job width W; false if the tables and K + 1
 // slots do not fit.
 template <class T, int RNT, bool REGH>
-bool stream_ring(StreamGeo& g, int min_slots = 0) {
+bool stream_ring(StreamGeo& g, int min_slots = 0) {  // REGH: no slot holds a pending band
   constexpr int V = int(16 / sizeof(T));
   g.nb = (g.n + kStreamR - 1) / kStreamR;
   // g.K: the plan's lookahead (tables.hpp stream_lookahead), at most nb - 1
@@ -858,20 +885,30 @@ bool run_stream(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, 
                 const T* rmult, const T* rrpiv, const T* rupper, int64_t level_nodes,
                 cudaStream_t s) {
   constexpr int RNT = ROWS ? 32 * chunk_pitch<T, CHR>() : 0;
-  auto go = [&](auto regh_c) {
-    constexpr bool REGH = decltype(regh_c)::value;
-    if (!stream_ring<T, RNT, REGH>(g)) return false;
+  auto go = [&](auto kr_c) {
+    constexpr int KR = decltype(kr_c)::value;
+    if (!stream_ring<T, RNT, (KR > 0)>(g)) return false;
     const size_t smem = stream_layout<T>(g, RNT).bytes;
-    auto kern = k_thomas_stream<T, NT, ROWS, CHR, REGH>;
+    auto kern = k_thomas_stream<T, NT, ROWS, CHR, KR>;
     set_smem_attr(reinterpret_cast<const void*>(kern), smem);
     const int grid = std::min(g.njobs, stream_sm_count());
     launch_pdl(kern, dim3(unsigned(grid)), dim3(NT + 32), smem, s, level_nodes, in, out, g, mult,
                rpiv, upper, rmult, rrpiv, rupper);
     return true;
   };
-  // fp32 with one lookahead band: the pending band lives in registers
-  if (sizeof(T) == 4 && std::min(g.K, g.nb - 1) <= 1) return go(std::true_type{});
-  return go(std::false_type{});
+  // one lookahead band: the pending band lives in registers (knob HGR_STREAM_KR:
+  // the most bands kept in registers; 2 fits the fp64 strips' 288 threads but
+  // measured slower than the shared-memory slots, 3.15 vs 2.98 ms of fp64 IPK
+  // per 1025^3 round trip; 0: always shared memory)
+  static const int kr_max = [] {
+    const char* v = std::getenv("HGR_STREAM_KR");
+    return v ? std::atoi(v) : 1;
+  }();
+  const int nb = (g.n + kStreamR - 1) / kStreamR;
+  const int k = std::max(1, std::min(g.K, nb - 1));  // the lookahead stream_ring settles on
+  if (k <= 1 && kr_max >= 1) return go(std::integral_constant<int, 1>{});
+  if (k == 2 && kr_max >= 2) return go(std::integral_constant<int, 2>{});
+  return go(std::integral_constant<int, 0>{});
 }
 
 template <class T, int CHR, int CW, int RWN, bool PROV>

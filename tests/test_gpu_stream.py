@@ -61,6 +61,27 @@ def test_stream_thomas_forced_lookahead(cuda, port, parity_log, monkeypatch, sha
     test_stream_thomas_vs_oracle(cuda, port, parity_log, monkeypatch, shape, dt, nonuniform)
 
 
+# two pending bands in registers (HGR_STREAM_KR=2: read once per process, so in
+# a child process)
+@pytest.mark.parametrize("shape", ["17x257x129", "129x129x129"])
+def test_stream_two_register_bands(cuda, shape):
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, HGR_STREAM_KR="2", CFG=shape)
+    out = subprocess.run([sys.executable, str(root / "tools" / "dbg_inplace.py"), shape, "f64"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = out.stdout.strip().splitlines()[-1]
+    err = float(line.split("out-of-place err")[1].split()[0])
+    assert err <= 1e-12 * 1.5, line  # dbg_inplace reports max-abs error (|u| <= 1.5)
+    import re
+    nans = re.findall(r"np\.int64\((\d+)\)", line)
+    assert nans and all(v == "0" for v in nans), line  # no NaN from the in-place runs
+
+
 # fp64 whole-plane pass with the pending bands corrected in place (off by default)
 PLANES64 = [c for c in CASES if c[1] == np.float64]
 
