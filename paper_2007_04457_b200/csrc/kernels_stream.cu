@@ -510,7 +510,7 @@ constexpr int ws_maxnreg(int nth) {
              : (16384 / (((nth / 32) + 3) / 4 * 32)) / 8 * 8;
 }
 
-template <class T, int CHR, int CW, int RWN, bool PROV>
+template <class T, int CHR, int CW, int RWN, bool PROV, int PC>
 __global__ void __maxnreg__(ws_maxnreg((CW + RWN + 1) * 32))
     k_thomas_planes_ws(const T* in, T* out, StreamGeo G, const T* __restrict__ mult,
                        const T* __restrict__ rpiv, const T* __restrict__ upper,
@@ -570,7 +570,7 @@ __global__ void __maxnreg__(ws_maxnreg((CW + RWN + 1) * 32))
   const int G0 = int(gridDim.x);
   const int myjobs = int(blockIdx.x) < G.njobs ? (G.njobs - int(blockIdx.x) + G0 - 1) / G0 : 0;
   const int64_t nitems = int64_t(myjobs) * nb;
-  const int P = G.ncols;  // row length == pitch == W
+  const int P = PC > 0 ? PC : G.ncols;  // row length == pitch == W (PC: compile time)
   ptx::pdl_wait();  // the planes are the previous launches' output
 
   if (wp == CW + RWN) {
@@ -911,7 +911,7 @@ bool run_stream(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, 
   return go(std::integral_constant<int, 0>{});
 }
 
-template <class T, int CHR, int CW, int RWN, bool PROV>
+template <class T, int CHR, int CW, int RWN, bool PROV, int PC = 0>
 bool run_planes_ws(const T* in, T* out, StreamGeo g, const T* mult, const T* rpiv, const T* upper,
                    const T* rmult, const T* rrpiv, const T* rupper, int64_t level_nodes,
                    cudaStream_t s) {
@@ -920,7 +920,8 @@ bool run_planes_ws(const T* in, T* out, StreamGeo g, const T* mult, const T* rpi
   // PROV (pending bands corrected in place in global memory): two slots suffice,
   // the column warps hand a slot back as soon as its band is in registers
   if (!stream_ring<T, RNT, true>(g, PROV ? 2 : 0)) return false;
-  auto kern = k_thomas_planes_ws<T, CHR, CW, RWN, PROV>;
+  if (PC > 0 && g.ncols != PC) return false;
+  auto kern = k_thomas_planes_ws<T, CHR, CW, RWN, PROV, PC>;
   // the ring as deep as one resident CTA allows (shared memory + registers)
   size_t smem = 0;
   for (;; --g.nslot) {
@@ -1066,12 +1067,17 @@ int launch_thomas_stream(T* src, T* dst, const int64_t c[3], const T* const mult
       return !v || v[0] != '0';
     }();
     if (ws && std::min(g.K, int((c[1] + kStreamR - 1) / kStreamR) - 1) <= 1) {
-#define HGR_WS(CHR, CW)                                                                          \
-  run_planes_ws<T, CHR, CW, 8, false>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2], upper[2], \
-                               level_nodes, s)
-      if (c[2] <= 32 * 5) ok = HGR_WS(5, 3);
-      else if (c[2] <= 32 * 9) ok = HGR_WS(9, 5);
-      else ok = HGR_WS(17, 9);
+#define HGR_WS(CHR, CW, PC)                                                                      \
+  run_planes_ws<T, CHR, CW, 8, false, PC>(src, dst, g, mult[1], rpiv[1], upper[1], mult[2], rpiv[2], \
+                                          upper[2], level_nodes, s)
+      // the 2^k+1 row lengths of the large levels at compile time (address and
+      // guard arithmetic folds), any other length at run time
+      if (c[2] == 513) ok = HGR_WS(17, 9, 513);
+      else if (c[2] == 257) ok = HGR_WS(9, 5, 257);
+      else if (c[2] == 129) ok = HGR_WS(5, 3, 129);
+      else if (c[2] <= 32 * 5) ok = HGR_WS(5, 3, 0);
+      else if (c[2] <= 32 * 9) ok = HGR_WS(9, 5, 0);
+      else ok = HGR_WS(17, 9, 0);
 #undef HGR_WS
     }
     if (ok) {
