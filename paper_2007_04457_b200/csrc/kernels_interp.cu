@@ -141,9 +141,9 @@ __device__ __forceinline__ void ldnc(const T* row, int pos, T (&v)[N]) {
 // SUB (in-place decompose): out = U - interp(C) at refined nodes, U at coarse
 // nodes, with U in place of the coefficients (every cell reads only its own U,
 // the coarse values come from C) and a non-finite check of every cell into flag.
-// EC: the extent of dims 1 and 2 at compile time for the large 2^k+1 cubes (0:
+// E1C, E2C: the extents of dims 1 and 2 at compile time for the large 2^k+1 shapes (0:
 // run time), so the address arithmetic folds
-template <class T, bool WITH, bool HASZ, bool SUB, int EC = 0>
+template <class T, bool WITH, bool HASZ, bool SUB, int E1C = 0, int E2C = 0>
 __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
     k_interp_march(const __grid_constant__ CUtensorMap mcoef, const __grid_constant__ CUtensorMap mC,
                    const __grid_constant__ CUtensorMap mZ, int64_t coef_off, int64_t c_off,
@@ -162,8 +162,8 @@ __global__ void __launch_bounds__(ICfg<T>::NT, ICfg<T>::MINB)
   uint64_t* barc = barf + NS;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = ptx::warp_id_uniform();
-  const int64_t e0 = a.e[0], e1 = EC ? EC : a.e[1], e2 = EC ? EC : a.e[2];
-  const int64_t c0 = a.c[0], c1 = EC ? (EC + 1) / 2 : a.c[1], c2 = EC ? (EC + 1) / 2 : a.c[2];
+  const int64_t e0 = a.e[0], e1 = E1C ? E1C : a.e[1], e2 = E2C ? E2C : a.e[2];
+  const int64_t c0 = a.c[0], c1 = E1C ? (E1C + 1) / 2 : a.c[1], c2 = E2C ? (E2C + 1) / 2 : a.c[2];
   int bid = blockIdx.x;
   const int t2i = bid % nt2;
   bid /= nt2;
@@ -486,8 +486,10 @@ void run_interp(const T* coef, T* out, const T* Cv, const T* Zv, const LevelArgs
                 cudaStream_t s, int s0, int* flag = nullptr) {
   using Cf = ICfg<T>;
   auto kern = k_interp_march<T, WITH, HASZ, SUB>;
-  if (a.e[1] == 1025 && a.e[2] == 1025) kern = k_interp_march<T, WITH, HASZ, SUB, 1025>;
-  else if (a.e[1] == 513 && a.e[2] == 513) kern = k_interp_march<T, WITH, HASZ, SUB, 513>;
+  if (a.e[1] == 1025 && a.e[2] == 1025) kern = k_interp_march<T, WITH, HASZ, SUB, 1025, 1025>;
+  else if (a.e[1] == 513 && a.e[2] == 513) kern = k_interp_march<T, WITH, HASZ, SUB, 513, 513>;
+  else if (a.e[1] == 513 && a.e[2] == 1025) kern = k_interp_march<T, WITH, HASZ, SUB, 513, 1025>;
+  else if (a.e[1] == 257 && a.e[2] == 513) kern = k_interp_march<T, WITH, HASZ, SUB, 257, 513>;
   set_smem_attr(reinterpret_cast<const void*>(kern), Cf::total);
   const int nt1 = int((a.c[1] - 1 + Cf::TW1 - 1) / Cf::TW1);
   const int nt2 = int((a.c[2] - 1 + Cf::TW2 - 1) / Cf::TW2);

@@ -166,9 +166,9 @@ __device__ __forceinline__ void loadV(const T* row, int ph, int base, T (&v)[NV]
   }
 }
 
-// EC: the extent of dims 1 and 2 at compile time (the 2^k+1 cubes of the
+// E1C, E2C: the extents of dims 1 and 2 at compile time (the 2^k+1 shapes of the
 // large levels; 0 = run time), so the address arithmetic folds
-template <class T, int MODE, int EC = 0>
+template <class T, int MODE, int E1C = 0, int E2C = 0>
 __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
     k_level_fused(const __grid_constant__ CUtensorMap map, int64_t map_off, T* __restrict__ coef_out,
                   T* __restrict__ zload, T* __restrict__ gather, T* __restrict__ side, LevelArgs<T> a,
@@ -188,8 +188,8 @@ __global__ void __launch_bounds__(LCfg<T>::NT, LCfg<T>::MINB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::bar_off);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = ptx::warp_id_uniform();
-  const int64_t e0 = a.e[0], e1 = EC ? EC : a.e[1], e2 = EC ? EC : a.e[2];
-  const int64_t c0 = a.c[0], c1 = EC ? (EC + 1) / 2 : a.c[1], c2 = EC ? (EC + 1) / 2 : a.c[2];
+  const int64_t e0 = a.e[0], e1 = E1C ? E1C : a.e[1], e2 = E2C ? E2C : a.e[2];
+  const int64_t c0 = a.c[0], c1 = E1C ? (E1C + 1) / 2 : a.c[1], c2 = E2C ? (E2C + 1) / 2 : a.c[2];
   const int64_t plane_sz = e1 * e2;
   int bid = blockIdx.x;
   const int t2i = bid % nt2;
@@ -916,8 +916,10 @@ void run_fused(const T* U, T* coef, T* z, T* gather, T* side, const LevelArgs<T>
                cudaStream_t s, int s0, T* face_ws) {
   using C = LCfg<T>;
   auto kern = k_level_fused<T, MODE>;
-  if (a.e[1] == 1025 && a.e[2] == 1025) kern = k_level_fused<T, MODE, 1025>;
-  else if (a.e[1] == 513 && a.e[2] == 513) kern = k_level_fused<T, MODE, 513>;
+  if (a.e[1] == 1025 && a.e[2] == 1025) kern = k_level_fused<T, MODE, 1025, 1025>;
+  else if (a.e[1] == 513 && a.e[2] == 513) kern = k_level_fused<T, MODE, 513, 513>;
+  else if (a.e[1] == 513 && a.e[2] == 1025) kern = k_level_fused<T, MODE, 513, 1025>;
+  else if (a.e[1] == 257 && a.e[2] == 513) kern = k_level_fused<T, MODE, 257, 513>;
   set_smem_attr(reinterpret_cast<const void*>(kern), C::total);
   const int nt1 = int((a.c[1] - 1 + C::TW1 - 1) / C::TW1);
   const int nt2 = int((a.c[2] - 1 + C::TW2 - 1) / C::TW2);
