@@ -7,6 +7,6 @@ for c in "$@"; do
     timeout 300 python bench.py --config $c --no-cpu-baseline --steps 20 2>/dev/null | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
-print('$c $VAR=$v', round(d['ms_per_step'],3), 'ms')"
+print('$c $VAR=$v', round(d['ms_per_step'],3), 'ms', {k: round(v['ms_per_step'],3) for k,v in d['kernels'].items()})"
   done
 done

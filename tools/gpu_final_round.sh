@@ -7,7 +7,7 @@ timeout 1500 python -m pytest tests -m gpu -q -rs > $O/pytest_gpu.log 2>&1; echo
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 for spec in 1025x1025x1025:f64:1025f64 1025x1025x1025:f32:1025f32 513x513x513:f32:513f32 257x513x1025:f64:aniso_nu_f64 513x513:f64:513sq_f64; do
   IFS=: read shp dt name <<< "$spec"
-  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/ncu_launches_$name.csv python tools/prof_one.py $shp $dt >> $O/ncu.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file $O/ncu_launches_$name.csv python tools/prof_one.py $shp $dt >> $O/ncu.log 2>&1
   python tools/ncu_summary.py $O/ncu_launches_$name.csv 1 200 > $O/ncu_launches_$name.summary.txt 2>&1
 done
 timeout 600 bash tools/ncu_one.sh $TAG/full_dec_f64 "k_level_fused" 0 1025x1025x1025 f64 >> $O/ncu.log 2>&1

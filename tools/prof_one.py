@@ -1,5 +1,8 @@
 """Autotune, then one warm-up + one measured round trip (for ncu launch lists);
-each round trip is preceded by a marker fill kernel."""
+each round trip is preceded by a marker fill kernel. The round trips run inside a
+profiler range (cudaProfilerStart/Stop): with `ncu --profile-from-start off` the
+tuner's candidate launches are neither profiled nor timed under the profiler,
+so the launch list shows the segment lengths bench.py runs with."""
 import sys
 sys.path.insert(0, '.')
 import torch
@@ -11,8 +14,11 @@ p_ = torch.empty_like(x)
 plan = hgr.Plan(g, dt)
 if '--no-tune' not in sys.argv:
     plan.autotune(x, p_)  # as bench.py does
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
 for _ in range(2):
     # marker launch (a fill kernel): the tools take the launches after the last one
     torch.ones(1, device='cuda')
     plan.decompose_into(x, p_); plan.recompose_into(p_, x, g.levels())
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
