@@ -42,6 +42,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "kernels_fused.cuh"
@@ -950,7 +951,11 @@ void run_fused(const T* U, T* coef, T* z, T* gather, T* side, const LevelArgs<T>
   }
   // two-phase faces for levels with large faces (one launch each below: the
   // small levels are launch-latency bound)
-  if (face_ws != nullptr && a.e[0] * a.e[1] >= (int64_t(1) << 18)) {
+  static const int64_t face2_min = [] {  // knob HGR_FACE2_MIN: smallest e0*e1 for two phases
+    const char* v = std::getenv("HGR_FACE2_MIN");
+    return v ? int64_t(std::atoll(v)) : int64_t(1) << 18;
+  }();
+  if (face_ws != nullptr && a.e[0] * a.e[1] >= face2_min) {
     T* R2 = face_ws;
     T* P2f = face_ws + a.e[0] * a.e[1];
     const int64_t n1 = std::max({a.e[1], 3 * (a.c[2] - 1), a.e[2] - 1});

@@ -346,6 +346,7 @@ class PlanT final : public Plan {
   // 3D IPK as streaming column passes (kernels_stream.cu), ahead of the band
   // kernels; knob HGR_THOMAS_STREAM=0 disables
   bool stream_thomas_ = true;
+  int64_t stream_min_ = 0;  // smallest level (coarse nodes) for the streaming passes
   TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
   std::vector<int> s0_dec_, s0_rec_, s0_int_;
@@ -366,6 +367,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   if (const char* v = std::getenv("HGR_AUTOTUNE")) auto_tune_pending_ = v[0] == '1';
   if (const char* v = std::getenv("HGR_THOMAS_BAND")) band_thomas_ = std::atoi(v);
   if (const char* v = std::getenv("HGR_THOMAS_STREAM")) stream_thomas_ = v[0] != '0';
+  if (const char* v = std::getenv("HGR_STREAM_MIN")) stream_min_ = std::atoll(v);
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   s0_dec_.assign(std::size_t(h.L) + 1, 0);
   s0_rec_.assign(std::size_t(h.L) + 1, 0);
@@ -664,7 +666,7 @@ template <class T>
 void PlanT<T>::thomas_all(int l, T* src, T* last_out, cudaStream_t s) {
   const LevelArgs<T>& a = args_[std::size_t(l)];
   const int64_t c[3] = {a.c[0], a.c[1], a.c[2]};
-  if (h.rank == 3 && stream_thomas_) {
+  if (h.rank == 3 && stream_thomas_ && c[0] * c[1] * c[2] >= stream_min_) {
     // dim 0 strips in place, then dims 1+2 (fp32 planes; fp64 strips + rows) into last_out
     prof_begin(kKindThomas, sz() * (sizeof(T) == 8 ? 6.0 : 4.0) * double(c[0] * c[1] * c[2]), s);
     const int nl = launch_thomas_stream<T>(src, last_out, c, a.mult, a.rpiv, a.upper,

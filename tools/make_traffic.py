@@ -5,8 +5,8 @@ import csv, io, json, re, sys, collections
 from pathlib import Path
 
 CLASSES = {  # bench kind -> (kernel-name regex, bench brackets per round trip)
-    "fused_decompose_level": (r"k_(level_(fused|face)|face_(slab|zload))<\w+, 0>", None),
-    "fused_recompose_level": (r"k_(level_(fused|face)|face_(slab|zload))<\w+, 2>", None),
+    "fused_decompose_level": (r"k_(level_(fused|face)|face_(slab|zload))<\w+, 0[,>]", None),
+    "fused_recompose_level": (r"k_(level_(fused|face)|face_(slab|zload))<\w+, 2[,>]", None),
     "recompose_interp": (r"k_interp_(march|face)", None),
     "thomas": (r"k_thomas_(lines|rows|long|stream|planes_ws|band)", None),
     "assembly": (r"k_(scatter|merge)_even", None),
