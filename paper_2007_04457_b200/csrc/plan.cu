@@ -346,7 +346,11 @@ class PlanT final : public Plan {
   // 3D IPK as streaming column passes (kernels_stream.cu), ahead of the band
   // kernels; knob HGR_THOMAS_STREAM=0 disables
   bool stream_thomas_ = true;
-  int64_t stream_min_ = 0;  // smallest level (coarse nodes) for the streaming passes
+  // smallest level (coarse nodes) for the streaming passes: fp64 levels below
+  // 2^20 run the three-pass kernels (257x513x1025 fp64: 2.083 -> 2.062 ms per
+  // round trip; 1025^3 fp64 unchanged); fp32 streams every level (the plane
+  // pass wins at every size). Knob HGR_STREAM_MIN.
+  int64_t stream_min_ = sizeof(T) == 8 ? int64_t(1) << 20 : 0;
   TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
   std::vector<int> s0_dec_, s0_rec_, s0_int_;

@@ -19,6 +19,14 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _stream_every_level(monkeypatch):
+    # fp64 levels under 2^20 coarse nodes take the three-pass kernels by default
+    # (plan.cu stream_min_); these shapes are small so that they cover the
+    # streaming passes, so switch the threshold off
+    monkeypatch.setenv("HGR_STREAM_MIN", "0")
+
+
 def _hgr():
     import paper_2007_04457_b200 as hgr
     return hgr

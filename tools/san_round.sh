@@ -1,6 +1,7 @@
 #!/bin/bash
 # compute-sanitizer over the streaming / face / level kernels on small shapes (dev aid)
 O=gpurun_out/${1:-san}; mkdir -p $O
+export HGR_STREAM_MIN=0  # every level through the streaming passes (fp64 default: >= 2^20 nodes)
 for t in memcheck synccheck racecheck; do
   for spec in 17x257x129:f64 17x257x129:f32 33x129x65:f64 65x65x65:f32; do
     IFS=: read shp dt <<< "$spec"
