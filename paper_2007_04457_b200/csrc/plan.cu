@@ -309,7 +309,7 @@ class PlanT final : public Plan {
   // levels with at least big_nodes_ nodes run the fused / TMA kernels, smaller
   // ones the one-thread-per-item kernels (tuning knob: HGR_BIG_LEVEL_NODES)
   bool big(int l) const { return h.node_count(l) >= big_nodes_; }
-  std::size_t big_nodes_ = std::size_t(1) << 15;
+  std::size_t big_nodes_ = 4096;
   int L() const { return h.L; }
 
   std::vector<LevelArgs<T>> args_;     // index l = 1..L (0 unused)
@@ -366,7 +366,9 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   h = hier;
   // 1D/2D levels are a few rows of fused tiles: the fused path wins from 4096
   // nodes (with programmatic launches), 3D levels from 2^15 (measured)
-  big_nodes_ = h.rank == 3 ? std::size_t(1) << 15 : std::size_t(4096);
+  // 4096 nodes for every rank (3D: 513^3 fp32 1.250 -> 1.242 ms, 1025^3 fp32
+  // 6.693 -> 6.685 ms against 2^15; 257x513x1025 fp64 unchanged)
+  big_nodes_ = std::size_t(4096);
   if (const char* v = std::getenv("HGR_BIG_LEVEL_NODES")) big_nodes_ = std::size_t(std::atoll(v));
   if (const char* v = std::getenv("HGR_AUTOTUNE")) auto_tune_pending_ = v[0] == '1';
   if (const char* v = std::getenv("HGR_THOMAS_BAND")) band_thomas_ = std::atoi(v);

@@ -202,7 +202,7 @@ FUSED_SHAPES = [(65, 65, 65), (33, 129, 65), (129, 33, 17), (17, 257, 129), (257
 @pytest.mark.parametrize("nonuniform", [False, True], ids=["uniform", "nonuniform"])
 @pytest.mark.parametrize("shape", FUSED_SHAPES, ids=lambda s: "x".join(map(str, s)))
 def test_fused_levels_vs_oracle(cuda, port, shape, nonuniform, dt):
-    """Sizes that take the fused level kernels (>= 2^15 nodes per level)."""
+    """Sizes that take the fused level kernels (>= 4096 nodes per level)."""
     import torch
     hgr = _hgr()
     g, coords = make_grid(hgr, shape, nonuniform, seed=300)
