@@ -46,27 +46,58 @@ int guarded(Fn&& fn) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // ---- plan cache for the one-shot entry points ------------------------------
+// A grid key stores the coordinates only where they are not the uniform 0..n-1
+// (the null-coordinate grid): 1D grids carry as many coordinates as data
+// values, so a lookup compares the caller's arrays in place (chunked over the
+// host copy pool, hostio.cu) instead of copying them into a fresh key per call.
 struct CacheKey {
   int dtype, device, rank;
   std::size_t n[3];
-  std::vector<double> coords;
-  bool operator==(const CacheKey& o) const {
-    return dtype == o.dtype && device == o.device && rank == o.rank && n[0] == o.n[0] &&
-           n[1] == o.n[1] && n[2] == o.n[2] && coords == o.coords;
-  }
+  std::vector<double> coords[3];  // empty: uniform (0..n-1)
 };
 
-CacheKey make_key(const hgr_grid_desc* g, int dtype) {
+struct GridView {  // the caller's grid as a lookup key (no copies)
+  int dtype, device, rank;
+  std::size_t n[3];
+  const double* coords[3];  // nullptr: uniform
+};
+
+GridView view_of(const hgr_grid_desc* g, int dtype) {
   hgrb::require(g != nullptr, "grid descriptor is null");
   hgrb::require(g->rank >= 1 && g->rank <= 3, "grid must have 1 to 3 dimensions");
+  GridView v{};
+  v.dtype = dtype;
+  cudaGetDevice(&v.device);
+  v.rank = g->rank;
+  for (int d = 0; d < 3; ++d) {
+    v.n[d] = d < g->rank ? g->extents[d] : 1;
+    v.coords[d] = d < g->rank && g->coords[d] && !hgrb::host_coords_iota(g->coords[d], g->extents[d])
+                      ? g->coords[d]
+                      : nullptr;
+  }
+  return v;
+}
+
+bool matches(const CacheKey& k, const GridView& v) {
+  if (k.dtype != v.dtype || k.device != v.device || k.rank != v.rank) return false;
+  for (int d = 0; d < 3; ++d) {
+    if (k.n[d] != v.n[d]) return false;
+    if (k.coords[d].empty() != (v.coords[d] == nullptr)) return false;
+  }
+  for (int d = 0; d < 3; ++d)
+    if (v.coords[d] && !hgrb::host_coords_equal(k.coords[d].data(), v.coords[d], v.n[d]))
+      return false;
+  return true;
+}
+
+CacheKey key_of(const GridView& v) {
   CacheKey k{};
-  k.dtype = dtype;
-  cudaGetDevice(&k.device);
-  k.rank = g->rank;
-  for (int d = 0; d < 3; ++d) k.n[d] = d < g->rank ? g->extents[d] : 1;
-  for (int d = 0; d < g->rank; ++d) {
-    k.coords.push_back(g->coords[d] ? 1.0 : 0.0);
-    if (g->coords[d]) k.coords.insert(k.coords.end(), g->coords[d], g->coords[d] + g->extents[d]);
+  k.dtype = v.dtype;
+  k.device = v.device;
+  k.rank = v.rank;
+  for (int d = 0; d < 3; ++d) {
+    k.n[d] = v.n[d];
+    if (v.coords[d]) k.coords[d].assign(v.coords[d], v.coords[d] + v.n[d]);
   }
   return k;
 }
@@ -105,13 +136,13 @@ struct Lease {
 };
 
 Lease cached_plan(const hgr_grid_desc* g, int dtype, cudaStream_t s = nullptr) {
-  CacheKey key = make_key(g, dtype);
+  const GridView view = view_of(g, dtype);
   std::shared_ptr<Plan> busy;
   {
     std::lock_guard<std::mutex> lock(g_cache_mu);
     auto it = g_cache.begin();
     for (; it != g_cache.end(); ++it)
-      if (it->key == key) break;
+      if (matches(it->key, view)) break;
     if (it != g_cache.end()) {
       g_cache.splice(g_cache.begin(), g_cache, it);
       for (auto& p : g_cache.front().pool) {
@@ -132,9 +163,9 @@ Lease cached_plan(const hgr_grid_desc* g, int dtype, cudaStream_t s = nullptr) {
     std::lock_guard<std::mutex> lock(g_cache_mu);
     auto it = g_cache.begin();
     for (; it != g_cache.end(); ++it)
-      if (it->key == key) break;
+      if (matches(it->key, view)) break;
     if (it == g_cache.end()) {
-      g_cache.push_front(CacheEntry{std::move(key), {}});
+      g_cache.push_front(CacheEntry{key_of(view), {}});
       it = g_cache.begin();
       if (g_cache.size() > kCacheCap) g_cache.pop_back();
     }

@@ -33,6 +33,7 @@ class CopyPool {
     static CopyPool pool;
     return pool;
   }
+  std::size_t threads() const { return workers_.size() + 1; }
   void copy(void* dst, const void* src, std::size_t bytes) {
     const std::size_t parts = std::min<std::size_t>(workers_.size() + 1, (bytes + (1 << 20) - 1) >> 20);
     if (parts <= 1) {
@@ -40,11 +41,18 @@ class CopyPool {
       return;
     }
     const std::size_t per = (bytes / parts + 63) & ~std::size_t(63);
-    auto part = [=](std::size_t k) {
+    run_parts(parts, [=](std::size_t k) {
       const std::size_t a = std::min(bytes, k * per), b = std::min(bytes, a + per);
       if (b > a) std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
-    };
-    std::lock_guard<std::mutex> one(call_mu_);  // one pooled copy at a time
+    });
+  }
+  // part(k) for k in [0, parts) on the workers and the calling thread
+  void run_parts(std::size_t parts, const std::function<void(std::size_t)>& part) {
+    if (parts <= 1) {
+      if (parts == 1) part(0);
+      return;
+    }
+    std::lock_guard<std::mutex> one(call_mu_);  // one pooled job at a time
     std::unique_lock<std::mutex> lk(mu_);
     {
       job_ = part;
@@ -109,6 +117,21 @@ class CopyPool {
   unsigned long gen_ = 0;
   bool stop_ = false;
 };
+
+// a predicate over [0, n) evaluated in chunks on the copy pool (large n only)
+bool all_chunks(std::size_t n, const std::function<bool(std::size_t, std::size_t)>& ok) {
+  constexpr std::size_t kMin = std::size_t(1) << 20;
+  auto& pool = CopyPool::get();
+  const std::size_t parts = std::min<std::size_t>(pool.threads(), (n + kMin - 1) / kMin);
+  if (parts <= 1) return ok(0, n);
+  const std::size_t per = (n + parts - 1) / parts;
+  std::vector<char> res(parts, 1);
+  pool.run_parts(parts, [&](std::size_t k) {
+    const std::size_t a = std::min(n, k * per), b = std::min(n, a + per);
+    res[k] = ok(a, b) ? 1 : 0;
+  });
+  return std::all_of(res.begin(), res.end(), [](char r) { return r != 0; });
+}
 
 bool is_pinned(const void* h) {
   cudaPointerAttributes at{};
@@ -194,6 +217,21 @@ void device_to_host(Plan& p, void* h, const void* d, std::size_t bytes, cudaStre
     const std::size_t off = i * kSlot, len = std::min(kSlot, bytes - off);
     pool.copy(static_cast<char*>(h) + off, slot(p, k), len);
   }
+}
+
+bool host_coords_iota(const double* c, std::size_t n) {
+  if (c == nullptr) return true;
+  return all_chunks(n, [c](std::size_t a, std::size_t b) {
+    for (std::size_t i = a; i < b; ++i)
+      if (c[i] != double(i)) return false;
+    return true;
+  });
+}
+
+bool host_coords_equal(const double* x, const double* y, std::size_t n) {
+  return all_chunks(n, [x, y](std::size_t a, std::size_t b) {
+    return std::memcmp(x + a, y + a, (b - a) * sizeof(double)) == 0;
+  });
 }
 
 }  // namespace hgrb

@@ -18,4 +18,11 @@ void host_to_device(Plan& p, void* d, const void* h, std::size_t bytes, cudaStre
 // d -> h after the work already on s; returns when h holds the data
 void device_to_host(Plan& p, void* h, const void* d, std::size_t bytes, cudaStream_t s);
 
+// grid-key helpers of the one-shot plan cache (capi.cu), chunked over the copy
+// pool: 1D grids carry as many coordinates as data values
+// c[i] == i for every i (null: the uniform grid)
+bool host_coords_iota(const double* c, std::size_t n);
+// bitwise equality of two coordinate arrays
+bool host_coords_equal(const double* x, const double* y, std::size_t n);
+
 }  // namespace hgrb

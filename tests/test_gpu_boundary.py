@@ -225,3 +225,26 @@ def test_apply_coefficients_vs_oracle(cuda, port, shape):
     want = port.interpolate_to_fine(coarse, shape, L, coords) + coeffs
     got = hgr.apply_coefficients(coarse, coeffs, g, L)
     assert np.abs(got - want).max() <= 1e-14
+
+
+@pytest.mark.parametrize("shape", [(2097153,), (33, 65, 129)], ids=["1d_2M", "3d"])
+def test_plan_cache_keys_by_coordinates(cuda, port, shape):
+    """The one-shot calls' plan cache keys a grid by its coordinates, compared in
+    place (chunked over host threads for long 1D grids): a uniform grid, a
+    non-uniform one and a copy of it with one coordinate moved share extents but
+    never a plan; each call matches the oracle on its own grid."""
+    hgr = _hgr()
+    c1 = [oracle.random_coords(n, 900 + d) for d, n in enumerate(shape)]
+    c2 = [c.copy() for c in c1]
+    last = c2[-1]
+    k = len(last) // 2 + 1
+    last[k] = 0.5 * (last[k] + last[k + 1])  # still strictly increasing
+    grids = {"uniform": (hgr.GridHierarchy.uniform(list(shape)), None),
+             "c1": (hgr.GridHierarchy(c1), c1), "c2": (hgr.GridHierarchy(c2), c2)}
+    u = _field(shape, np.float64, 5)
+    scale = float(np.abs(u).max())
+    for name in ("uniform", "c1", "c2", "uniform", "c2", "c1"):
+        g, coords = grids[name]
+        got = hgr.decompose(u.copy(), g).data
+        want = port.decompose(u, coords)
+        assert np.abs(got - want).max() / scale <= 1e-12, name
