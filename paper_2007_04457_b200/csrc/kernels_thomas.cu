@@ -409,7 +409,9 @@ template <class T, int CH>
 struct LongCfg {
   static constexpr int NT = 512, NC = NT, NP = NC * CH;
   static constexpr int TILE = NP + NC;  // one pad element per chunk: conflict-free chunk reads
-  static size_t smem() { return (size_t(2) * TILE + size_t(4) * NC) * sizeof(T); }
+  // two data tiles, the chunk summaries / products, and one window's three factor
+  // tables (same padded layout), prefetched with the data
+  static size_t smem() { return (size_t(5) * TILE + size_t(4) * NC) * sizeof(T); }
 };
 
 template <class T, int CH>
@@ -427,6 +429,9 @@ __global__ void __launch_bounds__(512, 1)
   T* sb = sf + NC;                         // [NC] backward chunk summaries
   T* sP = sb + NC;                         // [NC] forward chunk products
   T* sQ = sP + NC;                         // [NC] backward chunk products
+  T* fm = sQ + NC;                         // [3][TILE] next window's mult, rpiv, upper
+  T* fp = fm + TILE;
+  T* fu = fp + TILE;
   const int tid = threadIdx.x, q = tid, s0 = q * CH;
   const int64_t ngroups = rows * J;
   auto wstart = [&](int64_t j) { return J == 1 ? int64_t(0) : j * S - H; };
@@ -444,33 +449,57 @@ __global__ void __launch_bounds__(512, 1)
     }
     ptx::cp_async_commit();
   };
+  // window j's factors (zero past the line: padding positions never feed back),
+  // issued with a data prefetch so that their latency hides under the current
+  // group's solve (1D grids change window on every group)
+  auto prefetch_tab = [&](int64_t j) {
+    const int64_t ws = wstart(j);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const int i = k * NT + tid, pi = i + i / CH;
+      const int64_t pos = ws + i;
+      const bool om = pos >= 1 && pos < n, op = pos >= 0 && pos < n, ou = pos >= 0 && pos < n - 1;
+      ptx::cp_async_elem<int(sizeof(T))>(fm + pi, mult + (om ? pos - 1 : 0), om ? int(sizeof(T)) : 0);
+      ptx::cp_async_elem<int(sizeof(T))>(fp + pi, rpiv + (op ? pos : 0), op ? int(sizeof(T)) : 0);
+      ptx::cp_async_elem<int(sizeof(T))>(fu + pi, upper + (ou ? pos : 0), ou ? int(sizeof(T)) : 0);
+    }
+  };
 
   T tm[CH], tp[CH], tu[CH];
   int64_t cur_j = -1;
   int64_t g = blockIdx.x;
   ptx::pdl_wait();
-  if (g < ngroups) prefetch(g, 0);
+  if (g < ngroups) {
+    prefetch_tab(g / rows);
+    prefetch(g, 0);
+  }
   for (int it = 0; g < ngroups; g += gridDim.x, ++it) {
     const int b = it & 1;
     const int64_t j = g / rows, r = g - j * rows, ws = wstart(j);
-    if (j != cur_j) {  // this window's factors; padding positions never feed back
+    ptx::cp_async_wait_all();
+    __syncthreads();  // tile b (and window j's tables) complete; the previous group's store has read tile b^1
+    if (j != cur_j) {  // this window's factors, from the prefetched tables
       cur_j = j;
       T a = T(1), c = T(1);
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
-        const int64_t pos = ws + s0 + k;
-        tm[k] = (pos >= 1 && pos < n) ? mult[pos - 1] : T(0);
-        tp[k] = (pos >= 0 && pos < n) ? rpiv[pos] : T(0);
-        tu[k] = (pos >= 0 && pos < n - 1) ? upper[pos] : T(0);
+        tm[k] = fm[s0 + q + k];  // padded index i + i / CH
+        tp[k] = fp[s0 + q + k];
+        tu[k] = fu[s0 + q + k];
         a *= -tm[k];
         c *= -(tu[k] * tp[k]);
       }
       sP[q] = a;  // read by the scans after the barrier below
       sQ[q] = c;
     }
-    ptx::cp_async_wait_all();
-    __syncthreads();  // tile b complete; the previous group's store has read tile b^1
-    if (g + int64_t(gridDim.x) < ngroups) prefetch(g + gridDim.x, b ^ 1);
+    if (g + int64_t(gridDim.x) < ngroups) {
+      const int64_t jn = (g + int64_t(gridDim.x)) / rows;
+      if (jn != j) {  // the tables are overwritten: every thread has its factors
+        __syncthreads();
+        prefetch_tab(jn);
+      }
+      prefetch(g + gridDim.x, b ^ 1);
+    }
     T* t = tile + b * TILE;
     T x[CH];
 #pragma unroll
