@@ -350,6 +350,7 @@ class PlanT final : public Plan {
   // 2^20 run the three-pass kernels (257x513x1025 fp64: 2.083 -> 2.062 ms per
   // round trip; 1025^3 fp64 unchanged); fp32 streams every level (the plane
   // pass wins at every size). Knob HGR_STREAM_MIN.
+  std::size_t tune_top_ = 3;  // autotune: candidates measured per kernel (knob HGR_TUNE_TOP)
   int64_t stream_min_ = sizeof(T) == 8 ? int64_t(1) << 20 : 0;
   TailLevel<T>* tail_dev_ = nullptr;
   // tuned segment lengths per level (0: heuristic): decompose, recompose, interp
@@ -374,6 +375,7 @@ PlanT<T>::PlanT(const Hierarchy& hier) {
   if (const char* v = std::getenv("HGR_THOMAS_BAND")) band_thomas_ = std::atoi(v);
   if (const char* v = std::getenv("HGR_THOMAS_STREAM")) stream_thomas_ = v[0] != '0';
   if (const char* v = std::getenv("HGR_STREAM_MIN")) stream_min_ = std::atoll(v);
+  if (const char* v = std::getenv("HGR_TUNE_TOP")) tune_top_ = std::size_t(std::max(1, std::atoi(v)));
   dtype = sizeof(T) == 8 ? HGR_F64 : HGR_F32;
   s0_dec_.assign(std::size_t(h.L) + 1, 0);
   s0_rec_.assign(std::size_t(h.L) + 1, 0);
@@ -1035,7 +1037,7 @@ std::string PlanT<T>::autotune(const void* d_in, void* d_out, cudaStream_t s) {
   bool first = true;
   auto tune = [&](int l, const char* name, std::vector<SegChoice> cands, int dflt,
                   const std::function<void(int)>& run, int& slot) {
-    const std::size_t k = std::min<std::size_t>(3, cands.size());
+    const std::size_t k = std::min<std::size_t>(tune_top_, cands.size());
     double best = 0;
     int best_s0 = 0;
     std::string cj;
